@@ -1,0 +1,742 @@
+// engine.cu -- device orchestration: workspaces, streams, kernel dispatch over
+// (u,v), host<->device staging, and the NCCL row partitioner.
+#include "engine.hpp"
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace fpmm_b200 {
+
+#define CUDA_OK(x)                                                                              \
+  do {                                                                                          \
+    cudaError_t e_ = (x);                                                                       \
+    if (e_ != cudaSuccess)                                                                      \
+      throw Failure(FPMM_B200_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_));          \
+  } while (0)
+#define NCCL_OK(x)                                                                              \
+  do {                                                                                          \
+    ncclResult_t r_ = (x);                                                                      \
+    if (r_ != ncclSuccess)                                                                      \
+      throw Failure(FPMM_B200_ENCCL, std::string(#x) + ": " + ncclGetErrorString(r_));          \
+  } while (0)
+
+namespace {
+
+std::recursive_mutex g_mu;
+
+// grow-only device buffer
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  void* get(size_t need) {
+    if (need > bytes) {
+      if (ptr) cudaFree(ptr);
+      ptr = nullptr;
+      bytes = 0;
+      if (cudaMalloc(&ptr, std::max<size_t>(need, 256)) != cudaSuccess) {
+        cudaGetLastError();
+        throw Failure(FPMM_B200_ENOMEM, "device allocation of " + std::to_string(need) + " bytes failed");
+      }
+      bytes = std::max<size_t>(need, 256);
+    }
+    return ptr;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+  }
+};
+
+struct DeviceCtx {
+  int dev = -1;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[8] = {};
+  DevBuf apack, bpack, a, b, c, tmp, err;
+  void init(int d) {
+    dev = d;
+    CUDA_OK(cudaSetDevice(d));
+    CUDA_OK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    for (auto& e : ev) CUDA_OK(cudaEventCreate(&e));
+  }
+  void release() {
+    if (dev < 0) return;
+    cudaSetDevice(dev);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e), e = nullptr;
+    if (stream) cudaStreamDestroy(stream), stream = nullptr;
+    apack.release(), bpack.release(), a.release(), b.release(), c.release(), tmp.release(), err.release();
+    dev = -1;
+  }
+};
+
+std::vector<std::unique_ptr<DeviceCtx>> g_ctx;
+
+DeviceCtx& ctx(int dev) {
+  int count = 0;
+  CUDA_OK(cudaGetDeviceCount(&count));
+  if (dev < 0 || dev >= count)
+    throw Failure(FPMM_B200_EERROR, "device " + std::to_string(dev) + " out of range (" +
+                                        std::to_string(count) + " visible)");
+  if (g_ctx.size() < static_cast<size_t>(count)) g_ctx.resize(count);
+  if (!g_ctx[dev]) {
+    g_ctx[dev] = std::make_unique<DeviceCtx>();
+    g_ctx[dev]->init(dev);
+  }
+  CUDA_OK(cudaSetDevice(dev));
+  return *g_ctx[dev];
+}
+
+// ----------------------------------------------------------- (u,v) dispatch
+// warp tile per word pair: MT x NT DMMA tiles of 8x8 (<= 64 fp64 accumulators)
+template <typename F>
+void dispatch(int u, int v, F&& f) {
+#define FPMM_CASE(U, V, MT, NT) \
+  if (u == U && v == V) return f.template operator()<U, V, MT, NT>();
+  FPMM_CASE(1, 1, 8, 4)
+  FPMM_CASE(1, 2, 4, 4)
+  FPMM_CASE(2, 1, 4, 4)
+  FPMM_CASE(1, 3, 4, 2)
+  FPMM_CASE(3, 1, 4, 2)
+  FPMM_CASE(1, 4, 4, 2)
+  FPMM_CASE(4, 1, 4, 2)
+  FPMM_CASE(2, 2, 4, 2)
+  FPMM_CASE(2, 3, 2, 2)
+  FPMM_CASE(3, 2, 2, 2)
+  FPMM_CASE(2, 4, 2, 2)
+  FPMM_CASE(4, 2, 2, 2)
+#undef FPMM_CASE
+  throw Failure(FPMM_B200_EERROR, "unsupported word counts (u,v)=(" + std::to_string(u) + "," +
+                                      std::to_string(v) + "): need u,v <= 4 and uv <= 8");
+}
+
+DigitParams digit_params(u64 p, int w) {
+  const SignedWords s = signed_words(p, w);
+  DigitParams d;
+  d.p = static_cast<long long>(p);
+  d.half_p = static_cast<long long>(p / 2);
+  d.alpha = static_cast<long long>(s.alpha);
+  d.h = static_cast<long long>(s.half);
+  d.inv_alpha = 1.0 / static_cast<double>(s.alpha);
+  return d;
+}
+
+int grid_for(i64 items, int threads) {
+  const i64 blocks = (items + threads - 1) / threads;
+  return static_cast<int>(std::min<i64>(std::max<i64>(blocks, 1), 148 * 64));
+}
+
+// Everything the kernels need for one (m, k, n, p, u, v) problem.
+struct Job {
+  i64 m, k, n;
+  u64 p;
+  int u, v;
+  int BM = 0, BN = 0, MB = 0, NB = 0, KB = 0;
+  size_t apack_elems = 0, bpack_elems = 0;
+  i64 lambda_k = 0;
+  GemmParams gp{};
+  DigitParams da{}, db{};
+};
+
+Job make_job(i64 m, i64 k, i64 n, u64 p, int u, int v) {
+  Job j;
+  j.m = m, j.k = k, j.n = n, j.p = p, j.u = u, j.v = v;
+  dispatch(u, v, [&]<int U, int V, int MT, int NT>() {
+    using Cfg = GemmCfg<U, V, MT, NT>;
+    j.BM = Cfg::BM;
+    j.BN = Cfg::BN;
+    j.MB = static_cast<int>((m + Cfg::BM - 1) / Cfg::BM);
+    j.NB = static_cast<int>((n + Cfg::BN - 1) / Cfg::BN);
+    j.KB = static_cast<int>((k + 15) / 16);
+    j.apack_elems = static_cast<size_t>(j.MB) * j.KB * Cfg::kAElems;
+    j.bpack_elems = static_cast<size_t>(j.NB) * j.KB * Cfg::kBElems;
+  });
+  j.lambda_k = kernel_block(p, u, v, 4);
+  if (j.lambda_k < 4)
+    throw Failure(FPMM_B200_EINFEASIBLE, "no exact K-block >= 4 for (u,v)=(" + std::to_string(u) + "," +
+                                             std::to_string(v) + ") at p=" + std::to_string(p));
+  j.da = digit_params(p, u);
+  j.db = digit_params(p, v);
+  GemmParams& g = j.gp;
+  g.MB = j.MB, g.NB = j.NB, g.KB = j.KB;
+  g.m = m, g.n = n;
+  const i64 steps = j.lambda_k / 4;
+  g.red_every = static_cast<int>(std::min<i64>(steps, i64{1} << 30));
+  g.pf = static_cast<double>(p);
+  g.q = 1.0 / static_cast<double>(p);
+  g.p = p;
+  const u64 alpha = word_base(p, u) % p, beta = word_base(p, v) % p;
+  for (int i = 0; i < u; ++i)
+    for (int jj = 0; jj < v; ++jj) {
+      const u64 gm = mulmod(powmod(alpha, i, p), powmod(beta, jj, p), p);
+      g.gamma[i * v + jj] = gm;
+      g.gamma_sh[i * v + jj] = shoup(gm, p);
+    }
+  return j;
+}
+
+void launch_pack_a(const Job& j, const double* A, i64 lda, i64 rows, double* apack, int* err,
+                   cudaStream_t s) {
+  dispatch(j.u, j.v, [&]<int U, int V, int MT, int NT>() {
+    using Cfg = GemmCfg<U, V, MT, NT>;
+    const i64 mb = (rows + Cfg::BM - 1) / Cfg::BM;
+    const i64 mpad = mb * Cfg::BM;
+    const i64 items = (mpad / 2) * j.KB * 16;
+    pack_a_kernel<U, Cfg::BM><<<grid_for(items, 256), 256, 0, s>>>(A, lda, rows, j.k, j.KB, mpad, j.da,
+                                                                   apack, err);
+  });
+  CUDA_OK(cudaGetLastError());
+}
+
+void launch_pack_b(const Job& j, const double* B, i64 ldb, double* bpack, int* err, cudaStream_t s) {
+  dispatch(j.u, j.v, [&]<int U, int V, int MT, int NT>() {
+    using Cfg = GemmCfg<U, V, MT, NT>;
+    const i64 npad = static_cast<i64>(j.NB) * Cfg::BN;
+    const i64 items = (npad / 2) * j.KB * 16;
+    pack_b_kernel<V, Cfg::BN><<<grid_for(items, 256), 256, 0, s>>>(B, ldb, j.k, j.n, j.KB, npad, j.db,
+                                                                   bpack, err);
+  });
+  CUDA_OK(cudaGetLastError());
+}
+
+void launch_gemm(const Job& j, const double* apack, const double* bpack, double* C, i64 ldc, i64 rows,
+                 cudaStream_t s) {
+  GemmParams g = j.gp;
+  g.apack = apack;
+  g.bpack = bpack;
+  g.C = C;
+  g.ldc = ldc;
+  g.m = rows;
+  dispatch(j.u, j.v, [&]<int U, int V, int MT, int NT>() {
+    using Cfg = GemmCfg<U, V, MT, NT>;
+    g.MB = static_cast<int>((rows + Cfg::BM - 1) / Cfg::BM);
+    auto kern = mwgemm_kernel<U, V, MT, NT>;
+    static bool configured[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!configured[dev & 63]) {
+      CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem));
+      configured[dev & 63] = true;
+    }
+    const i64 tiles = static_cast<i64>(g.MB) * g.NB;
+    if (tiles > 0x7fffffff) throw Failure(FPMM_B200_EERROR, "problem too large for one launch");
+    kern<<<static_cast<unsigned>(tiles), Cfg::kThreads, Cfg::kSmem, s>>>(g);
+  });
+  CUDA_OK(cudaGetLastError());
+}
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms;
+}
+
+void check_err_flag(DeviceCtx& c, cudaStream_t s) {
+  int h = 0;
+  CUDA_OK(cudaMemcpyAsync(&h, c.err.ptr, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CUDA_OK(cudaStreamSynchronize(s));
+  if (h) throw Failure(FPMM_B200_ECONTRACT, "multiword product: inputs must be residues in [0, p)");
+}
+
+// Zero the rows x n block of C (k == 0 product).
+void zero_c(double* C, i64 ldc, i64 rows, i64 n, cudaStream_t s) {
+  if (rows > 0 && n > 0)
+    CUDA_OK(cudaMemset2DAsync(C, ldc * sizeof(double), 0, n * sizeof(double), rows, s));
+}
+
+}  // namespace
+
+void validate_product(u64 p, int u, int v, u64 lambda, i64 m, i64 k, i64 n, unsigned flags) {
+  if (m < 0 || k < 0 || n < 0) throw Failure(FPMM_B200_EERROR, "matrix dimensions must be nonnegative");
+  context_check(p, (flags & FPMM_B200_ALLOW_COMPOSITE) != 0);
+  check_mw_inputs(k, k, u, v, lambda, p);
+  if (flags & FPMM_B200_INPLACE_INVERSES) {
+    // scale_factors (multiword.hpp:76-86) inverts alpha (i > 0) and beta (j > 0)
+    auto invertible = [&](u64 base) {
+      u64 a = base % p, b = p;
+      while (b) {
+        const u64 t = a % b;
+        a = b;
+        b = t;
+      }
+      return a == 1;
+    };
+    if (u > 1 && !invertible(word_base(p, u)))
+      throw Failure(FPMM_B200_ENOINVERSE, "no inverse: gcd(alpha, p) > 1; use the workspace product variant");
+    if (v > 1 && !invertible(word_base(p, v)))
+      throw Failure(FPMM_B200_ENOINVERSE, "no inverse: gcd(beta, p) > 1; use the workspace product variant");
+  }
+}
+
+void product_device(const ProductArgs& a, int device, void* stream, fpmm_b200_timing* tm) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  validate_product(a.p, a.u, a.v, a.lambda, a.m, a.k, a.n, a.flags);
+  DeviceCtx& c = ctx(device);
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c.stream;
+  if (tm) *tm = fpmm_b200_timing{};
+  if (a.m == 0 || a.n == 0) return;
+  if (a.k == 0) {
+    zero_c(a.C, a.ldc, a.m, a.n, s);
+    if (!(a.flags & FPMM_B200_ASYNC)) CUDA_OK(cudaStreamSynchronize(s));
+    return;
+  }
+  const Job j = make_job(a.m, a.k, a.n, a.p, a.u, a.v);
+  double* apack = static_cast<double*>(c.apack.get(j.apack_elems * sizeof(double)));
+  double* bpack = static_cast<double*>(c.bpack.get(j.bpack_elems * sizeof(double)));
+  int* err = nullptr;
+  if (a.flags & FPMM_B200_CHECK_INPUTS) {
+    err = static_cast<int*>(c.err.get(sizeof(int)));
+    CUDA_OK(cudaMemsetAsync(err, 0, sizeof(int), s));
+  }
+  if (tm) CUDA_OK(cudaEventRecord(c.ev[0], s));
+  launch_pack_a(j, a.A, a.lda, a.m, apack, err, s);
+  launch_pack_b(j, a.B, a.ldb, bpack, err, s);
+  if (tm) CUDA_OK(cudaEventRecord(c.ev[1], s));
+  launch_gemm(j, apack, bpack, a.C, a.ldc, a.m, s);
+  if (tm) CUDA_OK(cudaEventRecord(c.ev[2], s));
+  if (err) check_err_flag(c, s);
+  if (tm) {
+    CUDA_OK(cudaEventSynchronize(c.ev[2]));
+    tm->pack_ms = elapsed(c.ev[0], c.ev[1]);
+    tm->gemm_ms = elapsed(c.ev[1], c.ev[2]);
+    tm->total_ms = elapsed(c.ev[0], c.ev[2]);
+    tm->lambda_k = j.lambda_k;
+    tm->launches = 3;
+    tm->ngpus = 1;
+  }
+  if (!(a.flags & FPMM_B200_ASYNC)) CUDA_OK(cudaStreamSynchronize(s));
+}
+
+// ------------------------------------------------------------- host buffers
+namespace {
+
+struct CommAll {
+  int n = 0;
+  std::vector<ncclComm_t> comms;
+  void ensure(int g) {
+    if (n == g) return;
+    for (auto cm : comms) ncclCommDestroy(cm);
+    comms.assign(g, nullptr);
+    std::vector<int> devs(g);
+    for (int i = 0; i < g; ++i) devs[i] = i;
+    NCCL_OK(ncclCommInitAll(comms.data(), g, devs.data()));
+    n = g;
+  }
+  void release() {
+    for (auto cm : comms) ncclCommDestroy(cm);
+    comms.clear();
+    n = 0;
+  }
+} g_all;
+
+// rows per partition: multiples of the GEMM's BM so every rank packs whole tiles
+i64 part_rows(i64 m, int parts, int bm) {
+  const i64 tiles = (m + bm - 1) / bm;
+  return ((tiles + parts - 1) / parts) * bm;
+}
+
+}  // namespace
+
+void product_host(const ProductArgs& a, int ngpus, fpmm_b200_timing* tm) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  validate_product(a.p, a.u, a.v, a.lambda, a.m, a.k, a.n, a.flags);
+  if (tm) *tm = fpmm_b200_timing{};
+  if (ngpus < 1) throw Failure(FPMM_B200_EERROR, "ngpus must be >= 1");
+  const int avail = device_count();
+  if (ngpus > avail)
+    throw Failure(FPMM_B200_EERROR, "requested " + std::to_string(ngpus) + " GPUs, " + std::to_string(avail) + " visible");
+  if (a.m == 0 || a.n == 0) return;
+  if (a.k == 0) {
+    for (i64 r = 0; r < a.m; ++r) std::memset(a.C + r * a.ldc, 0, sizeof(double) * a.n);
+    return;
+  }
+  const Job j = make_job(a.m, a.k, a.n, a.p, a.u, a.v);
+  const unsigned chk = a.flags & FPMM_B200_CHECK_INPUTS;
+
+  if (ngpus == 1) {
+    DeviceCtx& c = ctx(0);
+    cudaStream_t s = c.stream;
+    double* dA = static_cast<double*>(c.a.get(sizeof(double) * a.m * a.k));
+    double* dB = static_cast<double*>(c.b.get(sizeof(double) * a.k * a.n));
+    double* dC = static_cast<double*>(c.c.get(sizeof(double) * a.m * a.n));
+    double* apack = static_cast<double*>(c.apack.get(j.apack_elems * sizeof(double)));
+    double* bpack = static_cast<double*>(c.bpack.get(j.bpack_elems * sizeof(double)));
+    int* err = nullptr;
+    if (chk) {
+      err = static_cast<int*>(c.err.get(sizeof(int)));
+      CUDA_OK(cudaMemsetAsync(err, 0, sizeof(int), s));
+    }
+    CUDA_OK(cudaEventRecord(c.ev[0], s));
+    CUDA_OK(cudaMemcpy2DAsync(dA, a.k * 8, a.A, a.lda * 8, a.k * 8, a.m, cudaMemcpyHostToDevice, s));
+    CUDA_OK(cudaMemcpy2DAsync(dB, a.n * 8, a.B, a.ldb * 8, a.n * 8, a.k, cudaMemcpyHostToDevice, s));
+    CUDA_OK(cudaEventRecord(c.ev[1], s));
+    launch_pack_a(j, dA, a.k, a.m, apack, err, s);
+    launch_pack_b(j, dB, a.n, bpack, err, s);
+    CUDA_OK(cudaEventRecord(c.ev[2], s));
+    launch_gemm(j, apack, bpack, dC, a.n, a.m, s);
+    CUDA_OK(cudaEventRecord(c.ev[3], s));
+    CUDA_OK(cudaMemcpy2DAsync(a.C, a.ldc * 8, dC, a.n * 8, a.n * 8, a.m, cudaMemcpyDeviceToHost, s));
+    CUDA_OK(cudaEventRecord(c.ev[4], s));
+    CUDA_OK(cudaStreamSynchronize(s));
+    if (err) check_err_flag(c, s);
+    if (tm) {
+      tm->h2d_ms = elapsed(c.ev[0], c.ev[1]);
+      tm->pack_ms = elapsed(c.ev[1], c.ev[2]);
+      tm->gemm_ms = elapsed(c.ev[2], c.ev[3]);
+      tm->d2h_ms = elapsed(c.ev[3], c.ev[4]);
+      tm->total_ms = elapsed(c.ev[0], c.ev[4]);
+      tm->lambda_k = j.lambda_k;
+      tm->launches = 3;
+      tm->ngpus = 1;
+    }
+    return;
+  }
+
+  // ngpus > 1: contiguous row blocks of A / C per device; B words packed on
+  // device 0 and broadcast over NCCL (NVLink); each device writes its C rows
+  // straight back into the host matrix (row blocks are contiguous).
+  g_all.ensure(ngpus);
+  const i64 rows_per = part_rows(a.m, ngpus, j.BM);
+  std::vector<i64> r0(ngpus), rn(ngpus);
+  for (int g = 0; g < ngpus; ++g) {
+    r0[g] = std::min<i64>(a.m, g * rows_per);
+    rn[g] = std::min<i64>(a.m, r0[g] + rows_per) - r0[g];
+  }
+  std::vector<DeviceCtx*> cs(ngpus);
+  for (int g = 0; g < ngpus; ++g) cs[g] = &ctx(g);
+  std::vector<double*> dA(ngpus), dC(ngpus), apack(ngpus), bpack(ngpus);
+  std::vector<int*> errs(ngpus, nullptr);
+  double* dB0 = nullptr;
+  for (int g = 0; g < ngpus; ++g) {
+    DeviceCtx& c = *cs[g];
+    CUDA_OK(cudaSetDevice(g));
+    dA[g] = static_cast<double*>(c.a.get(sizeof(double) * std::max<i64>(rn[g], 1) * a.k));
+    dC[g] = static_cast<double*>(c.c.get(sizeof(double) * std::max<i64>(rn[g], 1) * a.n));
+    apack[g] = static_cast<double*>(c.apack.get(j.apack_elems * sizeof(double)));
+    bpack[g] = static_cast<double*>(c.bpack.get(j.bpack_elems * sizeof(double)));
+    if (chk) {
+      errs[g] = static_cast<int*>(c.err.get(sizeof(int)));
+      CUDA_OK(cudaMemsetAsync(errs[g], 0, sizeof(int), c.stream));
+    }
+    CUDA_OK(cudaEventRecord(c.ev[0], c.stream));
+    if (rn[g] > 0)
+      CUDA_OK(cudaMemcpy2DAsync(dA[g], a.k * 8, a.A + r0[g] * a.lda, a.lda * 8, a.k * 8, rn[g],
+                                cudaMemcpyHostToDevice, c.stream));
+    if (g == 0) {
+      dB0 = static_cast<double*>(c.b.get(sizeof(double) * a.k * a.n));
+      CUDA_OK(cudaMemcpy2DAsync(dB0, a.n * 8, a.B, a.ldb * 8, a.n * 8, a.k, cudaMemcpyHostToDevice, c.stream));
+    }
+    CUDA_OK(cudaEventRecord(c.ev[1], c.stream));
+    if (rn[g] > 0) launch_pack_a(j, dA[g], a.k, rn[g], apack[g], errs[g], c.stream);
+    if (g == 0) launch_pack_b(j, dB0, a.n, bpack[0], errs[0], c.stream);
+    CUDA_OK(cudaEventRecord(c.ev[2], c.stream));
+  }
+  NCCL_OK(ncclGroupStart());
+  for (int g = 0; g < ngpus; ++g) {
+    CUDA_OK(cudaSetDevice(g));
+    NCCL_OK(ncclBroadcast(bpack[0], bpack[g], j.bpack_elems, ncclDouble, 0, g_all.comms[g], cs[g]->stream));
+  }
+  NCCL_OK(ncclGroupEnd());
+  for (int g = 0; g < ngpus; ++g) {
+    DeviceCtx& c = *cs[g];
+    CUDA_OK(cudaSetDevice(g));
+    CUDA_OK(cudaEventRecord(c.ev[3], c.stream));
+    if (rn[g] > 0) launch_gemm(j, apack[g], bpack[g], dC[g], a.n, rn[g], c.stream);
+    CUDA_OK(cudaEventRecord(c.ev[4], c.stream));
+    if (rn[g] > 0)
+      CUDA_OK(cudaMemcpy2DAsync(a.C + r0[g] * a.ldc, a.ldc * 8, dC[g], a.n * 8, a.n * 8, rn[g],
+                                cudaMemcpyDeviceToHost, c.stream));
+    CUDA_OK(cudaEventRecord(c.ev[5], c.stream));
+  }
+  double h2d = 0, pack = 0, comm = 0, gemm = 0, d2h = 0, total = 0;
+  for (int g = 0; g < ngpus; ++g) {
+    DeviceCtx& c = *cs[g];
+    CUDA_OK(cudaSetDevice(g));
+    CUDA_OK(cudaStreamSynchronize(c.stream));
+    if (errs[g]) check_err_flag(c, c.stream);
+    h2d = std::max<double>(h2d, elapsed(c.ev[0], c.ev[1]));
+    pack = std::max<double>(pack, elapsed(c.ev[1], c.ev[2]));
+    comm = std::max<double>(comm, elapsed(c.ev[2], c.ev[3]));
+    gemm = std::max<double>(gemm, elapsed(c.ev[3], c.ev[4]));
+    d2h = std::max<double>(d2h, elapsed(c.ev[4], c.ev[5]));
+    total = std::max<double>(total, elapsed(c.ev[0], c.ev[5]));
+  }
+  if (tm) {
+    tm->h2d_ms = h2d, tm->pack_ms = pack, tm->comm_ms = comm, tm->gemm_ms = gemm, tm->d2h_ms = d2h;
+    tm->total_ms = total;
+    tm->lambda_k = j.lambda_k;
+    tm->launches = 2 * ngpus + 1;
+    tm->ngpus = ngpus;
+  }
+}
+
+void product_words_host(const double* Aw, i64 a_stride, i64 lda, u64 alpha, int u, const double* Bw,
+                        i64 b_stride, i64 ldb, u64 beta, int v, double* C, i64 ldc, i64 m, i64 k,
+                        i64 n, u64 p, u64 lambda, unsigned flags, fpmm_b200_timing* tm) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  validate_product(p, u, v, lambda, m, k, n, flags);
+  if (m == 0 || n == 0) {
+    if (tm) *tm = fpmm_b200_timing{};
+    return;
+  }
+  // words -> residues on the device (sum_i alpha^i w_i mod p), then the product
+  DeviceCtx& c = ctx(0);
+  cudaStream_t s = c.stream;
+  const size_t aw = static_cast<size_t>(u) * m * k, bw = static_cast<size_t>(v) * k * n;
+  double* dW = static_cast<double*>(c.tmp.get(sizeof(double) * std::max<size_t>(aw + bw, 1)));
+  double* dA = static_cast<double*>(c.a.get(sizeof(double) * std::max<i64>(m * k, 1)));
+  double* dB = static_cast<double*>(c.b.get(sizeof(double) * std::max<i64>(k * n, 1)));
+  double* dC = static_cast<double*>(c.c.get(sizeof(double) * m * n));
+  for (int i = 0; i < u; ++i)
+    CUDA_OK(cudaMemcpy2DAsync(dW + static_cast<size_t>(i) * m * k, k * 8, Aw + i * a_stride, lda * 8, k * 8, m,
+                              cudaMemcpyHostToDevice, s));
+  for (int i = 0; i < v; ++i)
+    CUDA_OK(cudaMemcpy2DAsync(dW + aw + static_cast<size_t>(i) * k * n, n * 8, Bw + i * b_stride, ldb * 8, n * 8,
+                              k, cudaMemcpyHostToDevice, s));
+  if (m * k > 0)
+    recompose_kernel<<<grid_for(m * k, 256), 256, 0, s>>>(dW, m * k, k, m, k, u, alpha % p, shoup(alpha % p, p), p, dA);
+  if (k * n > 0)
+    recompose_kernel<<<grid_for(k * n, 256), 256, 0, s>>>(dW + aw, k * n, n, k, n, v, beta % p, shoup(beta % p, p), p,
+                                                         dB);
+  CUDA_OK(cudaGetLastError());
+  ProductArgs pa{dA, k, dB, n, dC, n, m, k, n, p, u, v, lambda, flags & ~FPMM_B200_CHECK_INPUTS};
+  product_device(pa, 0, s, tm);
+  CUDA_OK(cudaMemcpy2DAsync(C, ldc * 8, dC, n * 8, n * 8, m, cudaMemcpyDeviceToHost, s));
+  CUDA_OK(cudaStreamSynchronize(s));
+}
+
+void decompose_device(const double* dM, i64 ld, i64 rows, i64 cols, u64 p, int u, double* dwords,
+                      i64 word_stride, u64* base, int device, void* stream) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (u < 1) throw Failure(FPMM_B200_EERROR, "decompose: word count must be positive");
+  const u64 alpha = word_base(p, u);
+  if (base) *base = alpha;
+  DeviceCtx& c = ctx(device);
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c.stream;
+  if (rows * cols == 0) return;
+  const double af = static_cast<double>(alpha);
+  decompose_ref_kernel<<<grid_for(rows * cols, 256), 256, 0, s>>>(dM, ld, rows, cols, u, af, 1.0 / af, dwords,
+                                                                  word_stride);
+  CUDA_OK(cudaGetLastError());
+  CUDA_OK(cudaStreamSynchronize(s));
+}
+
+void decompose_host(const double* M, i64 ld, i64 rows, i64 cols, u64 p, int u, double* words,
+                    i64 word_stride, u64* base) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (u < 1) throw Failure(FPMM_B200_EERROR, "decompose: word count must be positive");
+  DeviceCtx& c = ctx(0);
+  const i64 e = rows * cols;
+  if (e == 0) {
+    if (base) *base = word_base(p, u);
+    return;
+  }
+  double* dM = static_cast<double*>(c.a.get(sizeof(double) * e));
+  double* dW = static_cast<double*>(c.tmp.get(sizeof(double) * e * u));
+  CUDA_OK(cudaMemcpy2DAsync(dM, cols * 8, M, ld * 8, cols * 8, rows, cudaMemcpyHostToDevice, c.stream));
+  decompose_device(dM, cols, rows, cols, p, u, dW, e, base, 0, c.stream);
+  for (int i = 0; i < u; ++i)
+    CUDA_OK(cudaMemcpyAsync(words + i * word_stride, dW + static_cast<size_t>(i) * e, sizeof(double) * e,
+                            cudaMemcpyDeviceToHost, c.stream));
+  CUDA_OK(cudaStreamSynchronize(c.stream));
+}
+
+void accumulate_device(double* dC, i64 ldc, const double* dA, i64 lda, const double* dB, i64 ldb,
+                       i64 m, i64 w, i64 n, int device, void* stream) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (m < 0 || w < 0 || n < 0) throw Failure(FPMM_B200_EERROR, "accumulate: negative dimensions");
+  DeviceCtx& c = ctx(device);
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c.stream;
+  if (m == 0 || n == 0 || w == 0) return;
+  dim3 grid(static_cast<unsigned>((n + 63) / 64), static_cast<unsigned>((m + 63) / 64));
+  accumulate_kernel<<<grid, 128, 0, s>>>(dC, ldc, dA, lda, dB, ldb, m, w, n);
+  CUDA_OK(cudaGetLastError());
+  CUDA_OK(cudaStreamSynchronize(s));
+}
+
+void accumulate_host(double* C, i64 ldc, const double* A, i64 lda, const double* B, i64 ldb, i64 m,
+                     i64 w, i64 n) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (m <= 0 || n <= 0 || w <= 0) return;
+  DeviceCtx& c = ctx(0);
+  cudaStream_t s = c.stream;
+  double* dA = static_cast<double*>(c.a.get(sizeof(double) * m * w));
+  double* dB = static_cast<double*>(c.b.get(sizeof(double) * w * n));
+  double* dC = static_cast<double*>(c.c.get(sizeof(double) * m * n));
+  CUDA_OK(cudaMemcpy2DAsync(dA, w * 8, A, lda * 8, w * 8, m, cudaMemcpyHostToDevice, s));
+  CUDA_OK(cudaMemcpy2DAsync(dB, n * 8, B, ldb * 8, n * 8, w, cudaMemcpyHostToDevice, s));
+  CUDA_OK(cudaMemcpy2DAsync(dC, n * 8, C, ldc * 8, n * 8, m, cudaMemcpyHostToDevice, s));
+  accumulate_device(dC, n, dA, w, dB, n, m, w, n, 0, s);
+  CUDA_OK(cudaMemcpy2DAsync(C, ldc * 8, dC, n * 8, n * 8, m, cudaMemcpyDeviceToHost, s));
+  CUDA_OK(cudaStreamSynchronize(s));
+}
+
+// Alg 2.3 C <- C + A B mod p with C reduced: computed as the (1,1) fused
+// product of A B followed by a modular add of the old C (exact, same value).
+void block_gemm_mod_host(double* C, i64 ldc, const double* A, i64 lda, const double* B, i64 ldb,
+                         i64 m, i64 k, i64 n, u64 lambda, u64 p, unsigned flags) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  context_check(p, true);
+  if (m < 0 || k < 0 || n < 0) throw Failure(FPMM_B200_EERROR, "block_gemm_mod: dimension mismatch");
+  if (lambda < 1) throw Failure(FPMM_B200_EINFEASIBLE, "block size infeasible");
+  if (m == 0 || n == 0) return;
+  std::vector<double> T(static_cast<size_t>(m) * n);
+  // words bounded by p-1: the (1,1) product; lambda checked against the bound
+  const u64 lam = std::min<u64>(lambda, static_cast<u64>(std::max<i64>(k, 1)));
+  const u128 peak = static_cast<u128>(lam) * (p - 1) * (p - 1) + (p - 1);
+  if (peak > (u128{1} << kT))
+    throw Failure(FPMM_B200_EINFEASIBLE, "block_gemm_mod: lambda max(A) max(B) + p - 1 exceeds 2^t");
+  ProductArgs pa{A, lda, B, ldb, T.data(), n, m, k, n, p, 1, 1, 1, flags | FPMM_B200_ALLOW_COMPOSITE};
+  product_host(pa, 1, nullptr);
+  for (i64 r = 0; r < m; ++r)
+    for (i64 j = 0; j < n; ++j) {
+      u64 x = static_cast<u64>(C[r * ldc + j]) + static_cast<u64>(T[r * n + j]);
+      C[r * ldc + j] = static_cast<double>(x >= p ? x - p : x);
+    }
+}
+
+int device_count() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+// ------------------------------------------------- multi-process partitioner
+namespace {
+struct DistState {
+  ncclComm_t comm = nullptr;
+  int nranks = 0, rank = -1, device = -1;
+} g_dist;
+}  // namespace
+
+int nccl_id_size() { return static_cast<int>(sizeof(ncclUniqueId)); }
+
+void nccl_unique_id(void* id) {
+  ncclUniqueId uid;
+  NCCL_OK(ncclGetUniqueId(&uid));
+  std::memcpy(id, &uid, sizeof(uid));
+}
+
+void dist_init(const void* id, int nranks, int rank, int device) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (nranks < 1 || rank < 0 || rank >= nranks) throw Failure(FPMM_B200_EERROR, "dist_init: bad rank/size");
+  if (g_dist.comm) ncclCommDestroy(g_dist.comm), g_dist.comm = nullptr;
+  ctx(device);
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof(uid));
+  NCCL_OK(ncclCommInitRank(&g_dist.comm, nranks, uid, rank));
+  g_dist.nranks = nranks;
+  g_dist.rank = rank;
+  g_dist.device = device;
+}
+
+void dist_finalize() {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (g_dist.comm) ncclCommDestroy(g_dist.comm);
+  g_dist = DistState{};
+}
+
+void dist_rows(i64 m, int nranks, int rank, int u, int v, i64* row0, i64* rows) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) throw Failure(FPMM_B200_EERROR, "dist_rows: bad rank/size");
+  int bm = 64;
+  dispatch(u, v, [&]<int U, int V, int MT, int NT>() { bm = GemmCfg<U, V, MT, NT>::BM; });
+  const i64 per = part_rows(m, nranks, bm);
+  const i64 r0 = std::min<i64>(m, rank * per);
+  *row0 = r0;
+  *rows = std::min<i64>(m, r0 + per) - r0;
+}
+
+void dist_product_device(const double* dA_rows, i64 lda, const double* dB, i64 ldb, double* dC_rows,
+                         i64 ldc, double* dC_full, i64 ldc_full, i64 m, i64 k, i64 n, u64 p, int u,
+                         int v, u64 lambda, int root, void* stream, unsigned flags,
+                         fpmm_b200_timing* tm) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (!g_dist.comm) throw Failure(FPMM_B200_EERROR, "dist_mw_product: call fpmm_b200_dist_init first");
+  validate_product(p, u, v, lambda, m, k, n, flags);
+  if (root < 0 || root >= g_dist.nranks) throw Failure(FPMM_B200_EERROR, "dist_mw_product: bad root");
+  if (tm) *tm = fpmm_b200_timing{};
+  if (m == 0 || n == 0 || k == 0) {
+    if (k == 0 && m > 0 && n > 0) throw Failure(FPMM_B200_EERROR, "dist_mw_product: k == 0 unsupported");
+    return;
+  }
+  DeviceCtx& c = ctx(g_dist.device);
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c.stream;
+  const Job j = make_job(m, k, n, p, u, v);
+  i64 r0 = 0, rn = 0;
+  dist_rows(m, g_dist.nranks, g_dist.rank, u, v, &r0, &rn);
+  double* apack = static_cast<double*>(c.apack.get(j.apack_elems * sizeof(double)));
+  double* bpack = static_cast<double*>(c.bpack.get(j.bpack_elems * sizeof(double)));
+  int* err = nullptr;
+  if (flags & FPMM_B200_CHECK_INPUTS) {
+    err = static_cast<int*>(c.err.get(sizeof(int)));
+    CUDA_OK(cudaMemsetAsync(err, 0, sizeof(int), s));
+  }
+  CUDA_OK(cudaEventRecord(c.ev[0], s));
+  if (g_dist.rank == root) launch_pack_b(j, dB, ldb, bpack, err, s);
+  if (rn > 0) launch_pack_a(j, dA_rows, lda, rn, apack, err, s);
+  CUDA_OK(cudaEventRecord(c.ev[1], s));
+  NCCL_OK(ncclBroadcast(bpack, bpack, j.bpack_elems, ncclDouble, root, g_dist.comm, s));
+  CUDA_OK(cudaEventRecord(c.ev[2], s));
+  if (rn > 0) launch_gemm(j, apack, bpack, dC_rows, ldc, rn, s);
+  CUDA_OK(cudaEventRecord(c.ev[3], s));
+  int launches = (rn > 0 ? 2 : 0) + (g_dist.rank == root ? 1 : 0);
+  if (dC_full) {
+    // gather row blocks to root (grouped point-to-point; NCCL has no gather)
+    if (ldc != n || (g_dist.rank == root && ldc_full != n))
+      throw Failure(FPMM_B200_EERROR, "dist_mw_product: gather needs dense row blocks (ld == n)");
+    NCCL_OK(ncclGroupStart());
+    if (g_dist.rank == root) {
+      for (int r = 0; r < g_dist.nranks; ++r) {
+        i64 q0 = 0, qn = 0;
+        dist_rows(m, g_dist.nranks, r, u, v, &q0, &qn);
+        if (qn == 0) continue;
+        if (r == root) {
+          if (dC_full + q0 * ldc_full != dC_rows)
+            CUDA_OK(cudaMemcpyAsync(dC_full + q0 * ldc_full, dC_rows, sizeof(double) * qn * n,
+                                    cudaMemcpyDeviceToDevice, s));
+        } else {
+          NCCL_OK(ncclRecv(dC_full + q0 * ldc_full, static_cast<size_t>(qn * n), ncclDouble, r, g_dist.comm, s));
+        }
+      }
+    } else if (rn > 0) {
+      NCCL_OK(ncclSend(dC_rows, static_cast<size_t>(rn * n), ncclDouble, root, g_dist.comm, s));
+    }
+    NCCL_OK(ncclGroupEnd());
+  }
+  CUDA_OK(cudaEventRecord(c.ev[4], s));
+  if (err) check_err_flag(c, s);
+  if (!(flags & FPMM_B200_ASYNC) || tm) CUDA_OK(cudaStreamSynchronize(s));
+  if (tm) {
+    tm->pack_ms = elapsed(c.ev[0], c.ev[1]);
+    tm->comm_ms = elapsed(c.ev[1], c.ev[2]) + elapsed(c.ev[3], c.ev[4]);
+    tm->gemm_ms = elapsed(c.ev[2], c.ev[3]);
+    tm->total_ms = elapsed(c.ev[0], c.ev[4]);
+    tm->lambda_k = j.lambda_k;
+    tm->launches = launches;
+    tm->ngpus = g_dist.nranks;
+  }
+}
+
+void finalize_all() {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (g_dist.comm) ncclCommDestroy(g_dist.comm);
+  g_dist = DistState{};
+  g_all.release();
+  for (auto& c : g_ctx)
+    if (c) c->release();
+  g_ctx.clear();
+}
+
+}  // namespace fpmm_b200
