@@ -189,6 +189,17 @@ int fpmm_b200_dist_mw_product_device(const double* dA_rows, int64_t lda, const d
                                      int u, int v, uint64_t lambda, int root, void* stream,
                                      unsigned flags, fpmm_b200_timing* timing);
 
+/* ------------------------------------------------------ benchmark support */
+/* Uniform residues in [0,p) generated on the device (counter-based
+ * splitmix64 with rejection; for inputs too large for the host mt19937_64
+ * generator of mat.hpp:112-120).  Rows [row0, row0+rows) of the global
+ * matrix, so row-sharded ranks generate consistent slices.  Synchronous
+ * when stream is NULL. */
+int fpmm_b200_random_residues_device(double* dM, int64_t ld, int64_t rows, int64_t cols, int64_t row0,
+                                     uint64_t p, uint64_t seed, int device, void* stream);
+/* Measured FP64 tensor-pipe peak (TFLOP/s): a DMMA.8x8x4-only loop. */
+int fpmm_b200_fp64_peak(int device, int iters, double* tflops);
+
 /* release every device workspace, stream and communicator */
 int fpmm_b200_finalize(void);
 

@@ -33,7 +33,7 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfpmm_b200.so")
+LIB_PATH = os.environ.get("FPMM_B200_LIB") or os.path.join(HERE, "libfpmm_b200.so")
 T = 53  # FpContext<double>::t
 
 
@@ -145,6 +145,8 @@ def lib():
         "fpmm_b200_dist_mw_product_device": (i32, [vp, i64, vp, i64, vp, i64, vp, i64, i64, i64, i64,
                                                    u64, i32, i32, u64, i32, vp, C.c_uint,
                                                    C.POINTER(Timing)]),
+        "fpmm_b200_random_residues_device": (i32, [vp, i64, i64, i64, i64, u64, u64, i32, vp]),
+        "fpmm_b200_fp64_peak": (i32, [i32, i32, C.POINTER(C.c_double)]),
         "fpmm_b200_finalize": (i32, []),
     }
     for name, (res, args) in sig.items():
@@ -371,14 +373,19 @@ def decompose(M, u: int, F: FpContext) -> WordDecomposition:
     return WordDecomposition(base.value, [words[i] for i in range(u)])
 
 
-def _product(A, B, u, v, lam, F, variant, ngpus=1, flags=0, timing=None) -> np.ndarray:
+def _product(A, B, u, v, lam, F, variant, ngpus=1, flags=0, timing=None, out=None) -> np.ndarray:
     A = _f64(A)
     B = _f64(B)
     if A.shape[1] != B.shape[0]:
         raise Error("multiword product: dimension mismatch")
     m, k = A.shape
     n = B.shape[1]
-    Cm = np.empty((m, n), dtype=np.float64)
+    if out is not None:
+        if out.shape != (m, n) or out.dtype != np.float64 or not out.flags.c_contiguous:
+            raise Error("out must be a C-contiguous float64 (m, n) array")
+        Cm = out
+    else:
+        Cm = np.empty((m, n), dtype=np.float64)
     if not F.prime:
         flags |= ALLOW_COMPOSITE
     tm = timing if timing is not None else None
@@ -389,12 +396,13 @@ def _product(A, B, u, v, lam, F, variant, ngpus=1, flags=0, timing=None) -> np.n
 
 
 def mw_product(A, B, u: int, v: int, lambda_: int, F: FpContext, kernel=None, *, ngpus: int = 1,
-               flags: int = 0, timing: Optional[Timing] = None) -> np.ndarray:
+               flags: int = 0, timing: Optional[Timing] = None, out=None) -> np.ndarray:
     """multiword.hpp:133-139: C = A B mod p via the (u,v)-multiword product.
 
     ``kernel`` is accepted for signature parity (the fused sm_100a kernel is
-    always used); ``ngpus`` row-shards C over devices 0..ngpus-1."""
-    return _product(A, B, u, v, lambda_, F, PLAIN, ngpus, flags, timing)
+    always used); ``ngpus`` row-shards C over devices 0..ngpus-1; ``out``
+    (e.g. a pinned-memory array) receives C."""
+    return _product(A, B, u, v, lambda_, F, PLAIN, ngpus, flags, timing, out)
 
 
 def mw_product_workspace(A, B, u, v, lambda_, F, kernel=None, **kw) -> np.ndarray:
@@ -490,6 +498,17 @@ def kernel_by_name(name: str) -> Optional[GemmKernel]:
 
 
 # ----------------------------------------------------------- device tensors
+CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy
+
+
+def _stream_handle(stream):
+    """ctypes value for a torch stream: None -> the library's own stream; the
+    default (legacy) stream, whose handle is 0, -> cudaStreamLegacy."""
+    if stream is None:
+        return None
+    return stream.cuda_stream or CUDA_STREAM_LEGACY
+
+
 def _dev_ld(t) -> int:
     if t.dim() != 2 or t.stride(1) != 1:
         raise Error("device matrices must be 2-D row-major (stride(1) == 1)")
@@ -507,7 +526,7 @@ def mw_product_device(A, B, Cout, p: int, u: int, v: int, lambda_: int, *, varia
     if allow_composite:
         flags |= ALLOW_COMPOSITE
     dev = A.device.index
-    sp = stream.cuda_stream if stream is not None else None
+    sp = _stream_handle(stream)
     _check(lib().fpmm_b200_mw_product_device(A.data_ptr(), _dev_ld(A), B.data_ptr(), _dev_ld(B),
                                              Cout.data_ptr(), _dev_ld(Cout), m, k, n, p, u, v,
                                              lambda_, variant, dev, sp, flags,
@@ -518,7 +537,7 @@ def decompose_device(M, p: int, u: int, words, stream=None) -> int:
     """Reference-identical words of device matrix M into words (u x rows x cols)."""
     rows, cols = M.shape
     base = C.c_uint64()
-    sp = stream.cuda_stream if stream is not None else None
+    sp = _stream_handle(stream)
     _check(lib().fpmm_b200_decompose_device(M.data_ptr(), _dev_ld(M), rows, cols, p, u,
                                             words.data_ptr(), rows * cols, C.byref(base),
                                             M.device.index, sp))
@@ -528,9 +547,24 @@ def decompose_device(M, p: int, u: int, words, stream=None) -> int:
 def accumulate_device(Cm, A, B, stream=None) -> None:
     m, w = A.shape
     n = B.shape[1]
-    sp = stream.cuda_stream if stream is not None else None
+    sp = _stream_handle(stream)
     _check(lib().fpmm_b200_accumulate_device(Cm.data_ptr(), _dev_ld(Cm), A.data_ptr(), _dev_ld(A),
                                              B.data_ptr(), _dev_ld(B), m, w, n, A.device.index, sp))
+
+
+def random_residues_device(M, p: int, seed: int, row0: int = 0, stream=None) -> None:
+    """Fill device tensor M (rows row0.. of a global matrix) with uniform residues in [0,p)."""
+    rows, cols = M.shape
+    sp = _stream_handle(stream)
+    _check(lib().fpmm_b200_random_residues_device(M.data_ptr(), _dev_ld(M), rows, cols, row0, p,
+                                                  seed, M.device.index, sp))
+
+
+def fp64_peak(device: int = 0, iters: int = 20000) -> float:
+    """Measured FP64 tensor-pipe (DMMA) peak of `device` in TFLOP/s."""
+    out = C.c_double()
+    _check(lib().fpmm_b200_fp64_peak(device, iters, C.byref(out)))
+    return out.value
 
 
 def device_count() -> int:

@@ -233,6 +233,15 @@ int fpmm_b200_dist_mw_product_device(const double* dA_rows, int64_t lda, const d
   });
 }
 
+int fpmm_b200_random_residues_device(double* dM, int64_t ld, int64_t rows, int64_t cols, int64_t row0,
+                                     uint64_t p, uint64_t seed, int device, void* stream) {
+  return guarded([&] { random_residues_device(dM, ld, rows, cols, row0, p, seed, device, stream); });
+}
+
+int fpmm_b200_fp64_peak(int device, int iters, double* tflops) {
+  return guarded([&] { *tflops = fp64_peak_tflops(device, iters); });
+}
+
 int fpmm_b200_finalize(void) {
   return guarded([&] { finalize_all(); });
 }

@@ -3,7 +3,7 @@
 #include "engine.hpp"
 
 #include <cuda_runtime.h>
-#include <nccl.h>
+#include "nccl_loader.hpp"
 
 #include <algorithm>
 #include <cstring>
@@ -26,7 +26,7 @@ namespace fpmm_b200 {
   do {                                                                                          \
     ncclResult_t r_ = (x);                                                                      \
     if (r_ != ncclSuccess)                                                                      \
-      throw Failure(FPMM_B200_ENCCL, std::string(#x) + ": " + ncclGetErrorString(r_));          \
+      throw Failure(FPMM_B200_ENCCL, std::string(#x) + ": " + nccl().GetErrorString(r_));          \
   } while (0)
 
 namespace {
@@ -324,15 +324,15 @@ struct CommAll {
   std::vector<ncclComm_t> comms;
   void ensure(int g) {
     if (n == g) return;
-    for (auto cm : comms) ncclCommDestroy(cm);
+    for (auto cm : comms) nccl().CommDestroy(cm);
     comms.assign(g, nullptr);
     std::vector<int> devs(g);
     for (int i = 0; i < g; ++i) devs[i] = i;
-    NCCL_OK(ncclCommInitAll(comms.data(), g, devs.data()));
+    NCCL_OK(nccl().CommInitAll(comms.data(), g, devs.data()));
     n = g;
   }
   void release() {
-    for (auto cm : comms) ncclCommDestroy(cm);
+    for (auto cm : comms) nccl().CommDestroy(cm);
     comms.clear();
     n = 0;
   }
@@ -440,12 +440,12 @@ void product_host(const ProductArgs& a, int ngpus, fpmm_b200_timing* tm) {
     if (g == 0) launch_pack_b(j, dB0, a.n, bpack[0], errs[0], c.stream);
     CUDA_OK(cudaEventRecord(c.ev[2], c.stream));
   }
-  NCCL_OK(ncclGroupStart());
+  NCCL_OK(nccl().GroupStart());
   for (int g = 0; g < ngpus; ++g) {
     CUDA_OK(cudaSetDevice(g));
-    NCCL_OK(ncclBroadcast(bpack[0], bpack[g], j.bpack_elems, ncclDouble, 0, g_all.comms[g], cs[g]->stream));
+    NCCL_OK(nccl().Broadcast(bpack[0], bpack[g], j.bpack_elems, ncclDouble, 0, g_all.comms[g], cs[g]->stream));
   }
-  NCCL_OK(ncclGroupEnd());
+  NCCL_OK(nccl().GroupEnd());
   for (int g = 0; g < ngpus; ++g) {
     DeviceCtx& c = *cs[g];
     CUDA_OK(cudaSetDevice(g));
@@ -604,6 +604,36 @@ void block_gemm_mod_host(double* C, i64 ldc, const double* A, i64 lda, const dou
     }
 }
 
+void random_residues_device(double* dM, i64 ld, i64 rows, i64 cols, i64 row0, u64 p, u64 seed, int device,
+                            void* stream) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (p < 2) throw Failure(FPMM_B200_EERROR, "random_residues: p must exceed 1");
+  DeviceCtx& c = ctx(device);
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c.stream;
+  if (rows * cols == 0) return;
+  const u64 kMax = ~u64{0};
+  random_residues_kernel<<<grid_for(rows * cols, 256), 256, 0, s>>>(dM, ld, rows, cols, row0, p, kMax - kMax % p, seed);
+  CUDA_OK(cudaGetLastError());
+  if (!stream) CUDA_OK(cudaStreamSynchronize(s));
+}
+
+double fp64_peak_tflops(int device, int iters) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  DeviceCtx& c = ctx(device);
+  int sms = 0;
+  CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  double* out = static_cast<double*>(c.err.get(4096));
+  const int blocks = sms * 4;
+  dmma_peak_kernel<<<blocks, 256, 0, c.stream>>>(iters, out);  // warm-up
+  CUDA_OK(cudaEventRecord(c.ev[0], c.stream));
+  dmma_peak_kernel<<<blocks, 256, 0, c.stream>>>(iters, out);
+  CUDA_OK(cudaEventRecord(c.ev[1], c.stream));
+  CUDA_OK(cudaEventSynchronize(c.ev[1]));
+  const double ms = elapsed(c.ev[0], c.ev[1]);
+  const double flops = 2.0 * 256.0 * 8.0 * iters * blocks * 8.0;  // 8 warps per block
+  return flops / (ms * 1e-3) / 1e12;
+}
+
 int device_count() {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess) {
@@ -625,18 +655,18 @@ int nccl_id_size() { return static_cast<int>(sizeof(ncclUniqueId)); }
 
 void nccl_unique_id(void* id) {
   ncclUniqueId uid;
-  NCCL_OK(ncclGetUniqueId(&uid));
+  NCCL_OK(nccl().GetUniqueId(&uid));
   std::memcpy(id, &uid, sizeof(uid));
 }
 
 void dist_init(const void* id, int nranks, int rank, int device) {
   std::lock_guard<std::recursive_mutex> lk(g_mu);
   if (nranks < 1 || rank < 0 || rank >= nranks) throw Failure(FPMM_B200_EERROR, "dist_init: bad rank/size");
-  if (g_dist.comm) ncclCommDestroy(g_dist.comm), g_dist.comm = nullptr;
+  if (g_dist.comm) nccl().CommDestroy(g_dist.comm), g_dist.comm = nullptr;
   ctx(device);
   ncclUniqueId uid;
   std::memcpy(&uid, id, sizeof(uid));
-  NCCL_OK(ncclCommInitRank(&g_dist.comm, nranks, uid, rank));
+  NCCL_OK(nccl().CommInitRank(&g_dist.comm, nranks, uid, rank));
   g_dist.nranks = nranks;
   g_dist.rank = rank;
   g_dist.device = device;
@@ -644,7 +674,7 @@ void dist_init(const void* id, int nranks, int rank, int device) {
 
 void dist_finalize() {
   std::lock_guard<std::recursive_mutex> lk(g_mu);
-  if (g_dist.comm) ncclCommDestroy(g_dist.comm);
+  if (g_dist.comm) nccl().CommDestroy(g_dist.comm);
   g_dist = DistState{};
 }
 
@@ -687,7 +717,7 @@ void dist_product_device(const double* dA_rows, i64 lda, const double* dB, i64 l
   if (g_dist.rank == root) launch_pack_b(j, dB, ldb, bpack, err, s);
   if (rn > 0) launch_pack_a(j, dA_rows, lda, rn, apack, err, s);
   CUDA_OK(cudaEventRecord(c.ev[1], s));
-  NCCL_OK(ncclBroadcast(bpack, bpack, j.bpack_elems, ncclDouble, root, g_dist.comm, s));
+  NCCL_OK(nccl().Broadcast(bpack, bpack, j.bpack_elems, ncclDouble, root, g_dist.comm, s));
   CUDA_OK(cudaEventRecord(c.ev[2], s));
   if (rn > 0) launch_gemm(j, apack, bpack, dC_rows, ldc, rn, s);
   CUDA_OK(cudaEventRecord(c.ev[3], s));
@@ -696,7 +726,7 @@ void dist_product_device(const double* dA_rows, i64 lda, const double* dB, i64 l
     // gather row blocks to root (grouped point-to-point; NCCL has no gather)
     if (ldc != n || (g_dist.rank == root && ldc_full != n))
       throw Failure(FPMM_B200_EERROR, "dist_mw_product: gather needs dense row blocks (ld == n)");
-    NCCL_OK(ncclGroupStart());
+    NCCL_OK(nccl().GroupStart());
     if (g_dist.rank == root) {
       for (int r = 0; r < g_dist.nranks; ++r) {
         i64 q0 = 0, qn = 0;
@@ -707,13 +737,13 @@ void dist_product_device(const double* dA_rows, i64 lda, const double* dB, i64 l
             CUDA_OK(cudaMemcpyAsync(dC_full + q0 * ldc_full, dC_rows, sizeof(double) * qn * n,
                                     cudaMemcpyDeviceToDevice, s));
         } else {
-          NCCL_OK(ncclRecv(dC_full + q0 * ldc_full, static_cast<size_t>(qn * n), ncclDouble, r, g_dist.comm, s));
+          NCCL_OK(nccl().Recv(dC_full + q0 * ldc_full, static_cast<size_t>(qn * n), ncclDouble, r, g_dist.comm, s));
         }
       }
     } else if (rn > 0) {
-      NCCL_OK(ncclSend(dC_rows, static_cast<size_t>(rn * n), ncclDouble, root, g_dist.comm, s));
+      NCCL_OK(nccl().Send(dC_rows, static_cast<size_t>(rn * n), ncclDouble, root, g_dist.comm, s));
     }
-    NCCL_OK(ncclGroupEnd());
+    NCCL_OK(nccl().GroupEnd());
   }
   CUDA_OK(cudaEventRecord(c.ev[4], s));
   if (err) check_err_flag(c, s);
@@ -731,7 +761,7 @@ void dist_product_device(const double* dA_rows, i64 lda, const double* dB, i64 l
 
 void finalize_all() {
   std::lock_guard<std::recursive_mutex> lk(g_mu);
-  if (g_dist.comm) ncclCommDestroy(g_dist.comm);
+  if (g_dist.comm) nccl().CommDestroy(g_dist.comm);
   g_dist = DistState{};
   g_all.release();
   for (auto& c : g_ctx)

@@ -47,6 +47,9 @@ void block_gemm_mod_host(double* C, i64 ldc, const double* A, i64 lda, const dou
                          i64 m, i64 k, i64 n, u64 lambda, u64 p, unsigned flags);
 
 int device_count();
+void random_residues_device(double* dM, i64 ld, i64 rows, i64 cols, i64 row0, u64 p, u64 seed, int device,
+                            void* stream);
+double fp64_peak_tflops(int device, int iters);
 void finalize_all();
 
 // multi-process partitioner

@@ -400,3 +400,49 @@ __global__ void __launch_bounds__(128) accumulate_kernel(double* __restrict__ C,
 }
 
 }  // namespace fpmm_b200
+
+namespace fpmm_b200 {
+
+// Device-side synthetic residues for large benchmarks: element e of a
+// rows x cols slice starting at global row row0 (global index g = (row0+i)*cols + j) is the first draw r = splitmix64(seed ^ (g * 2^8 + t)),
+// t = 0, 1, ..., below reject_at (the largest multiple of p), reduced mod p:
+// uniform on [0,p), deterministic, independent of launch geometry.
+__device__ __forceinline__ unsigned long long splitmix64(unsigned long long z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+__global__ void random_residues_kernel(double* __restrict__ M, i64 ld, i64 rows, i64 cols,
+                                       i64 row0, unsigned long long p, unsigned long long reject_at,
+                                       unsigned long long seed) {
+  const i64 total = rows * cols;
+  for (i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 i = e / cols, j = e % cols;
+    const unsigned long long g = static_cast<unsigned long long>((row0 + i) * cols + j);  // global index
+    unsigned long long t = 0, r;
+    do r = splitmix64(seed ^ ((g << 8) + t++));
+    while (r >= reject_at);
+    M[i * ld + j] = static_cast<double>(r % p);
+  }
+}
+
+// FP64 tensor-pipe peak probe: 8 independent DMMA.8x8x4 chains per warp.
+__global__ void __launch_bounds__(256) dmma_peak_kernel(int iters, double* out) {
+  double d[8][2];
+  const double a = 1.0 + threadIdx.x * 1e-3, b = 1.0 - threadIdx.x * 1e-3;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) d[c][0] = c, d[c][1] = -c;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) dev::dmma884(d[c][0], d[c][1], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) s += d[c][0] + d[c][1];
+  if (s == 1234.5) out[threadIdx.x] = s;
+}
+
+}  // namespace fpmm_b200

@@ -1,0 +1,48 @@
+"""Summarise an ncu --set full report into the metrics we quote (JSON to stdout).
+
+python tools/ncu_summary.py gpurun_out/prof.ncu-rep [label]
+"""
+import csv
+import io
+import json
+import subprocess
+import sys
+
+KEYS = [
+    "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__ops_path_tensor_src_fp64.sum.per_second",
+    "sm__ops_path_tensor_src_fp64.sum.peak_sustained_elapsed.per_second",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm__cycles_elapsed.avg.per_second",
+    "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+    "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "lts__t_bytes.sum",
+    "smsp__inst_executed.sum", "launch__shared_mem_per_block_dynamic",
+    "sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+]
+
+
+def main():
+    rep = sys.argv[1]
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True,
+                         check=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    res = []
+    for r in rows[2:]:
+        d = {"kernel": r[hdr.index("Kernel Name")] if "Kernel Name" in hdr else None}
+        for key in KEYS:
+            if key in hdr:
+                i = hdr.index(key)
+                d[key] = {"value": r[i], "unit": units[i]}
+        res.append(d)
+    print(json.dumps({"report": rep, "label": sys.argv[2] if len(sys.argv) > 2 else "", "launches": res},
+                     indent=1))
+
+
+if __name__ == "__main__":
+    main()
