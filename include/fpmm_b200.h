@@ -46,6 +46,12 @@ typedef enum {
 #define FPMM_B200_INPLACE_INVERSES 0x4u /* mw_product semantics: require alpha, beta invertible mod p
                                            (multiword.hpp:76-86); NoInverseError otherwise */
 #define FPMM_B200_BCAST_RAW_B 0x8u     /* multi-GPU: broadcast raw B and pack locally (default: B words) */
+/* engine selection (same results, different tensor-core path):
+ *   DMMA: the paper's FP64 multiword product on the FP64 tensor pipe (mma.sync .f64)
+ *   I8  : base-256 multiword words on tcgen05.mma.kind::i8 (int32 TMEM accumulators)
+ * neither flag = the library default (DMMA) */
+#define FPMM_B200_ENGINE_DMMA 0x10u
+#define FPMM_B200_ENGINE_I8 0x20u
 
 /* product variants (multiword.hpp:113-254); all map to the same fused kernel */
 typedef enum {

@@ -69,6 +69,8 @@ ALLOW_COMPOSITE = 0x1
 CHECK_INPUTS = 0x2
 INPLACE_INVERSES = 0x4
 BCAST_RAW_B = 0x8
+ENGINE_DMMA = 0x10  # FP64 multiword on the FP64 tensor pipe (DMMA)
+ENGINE_I8 = 0x20    # base-256 multiword on tcgen05.mma.kind::i8 (TMEM int32 accumulators)
 ASYNC = 0x100
 PLAIN, WORKSPACE, CONCAT = 0, 1, 2
 

@@ -12,6 +12,7 @@
 #include <string>
 #include <vector>
 
+#include "i8engine.cuh"
 #include "kernels.cuh"
 
 namespace fpmm_b200 {
@@ -58,21 +59,32 @@ struct DevBuf {
 };
 
 struct DeviceCtx {
+  static constexpr int kChunks = 8;  // host-path pipeline depth
   int dev = -1;
-  cudaStream_t stream = nullptr;
-  cudaEvent_t ev[8] = {};
+  cudaStream_t stream = nullptr, s_in = nullptr, s_out = nullptr;
+  cudaEvent_t ev[8] = {}, ev_in[kChunks] = {}, ev_out[kChunks] = {};
   DevBuf apack, bpack, a, b, c, tmp, err;
   void init(int d) {
     dev = d;
     CUDA_OK(cudaSetDevice(d));
     CUDA_OK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    CUDA_OK(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
+    CUDA_OK(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
     for (auto& e : ev) CUDA_OK(cudaEventCreate(&e));
+    for (auto& e : ev_in) CUDA_OK(cudaEventCreate(&e));
+    for (auto& e : ev_out) CUDA_OK(cudaEventCreate(&e));
   }
   void release() {
     if (dev < 0) return;
     cudaSetDevice(dev);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e), e = nullptr;
+    for (auto& e : ev_in)
+      if (e) cudaEventDestroy(e), e = nullptr;
+    for (auto& e : ev_out)
+      if (e) cudaEventDestroy(e), e = nullptr;
+    if (s_in) cudaStreamDestroy(s_in), s_in = nullptr;
+    if (s_out) cudaStreamDestroy(s_out), s_out = nullptr;
     if (stream) cudaStreamDestroy(stream), stream = nullptr;
     apack.release(), bpack.release(), a.release(), b.release(), c.release(), tmp.release(), err.release();
     dev = -1;
@@ -136,18 +148,74 @@ int grid_for(i64 items, int threads) {
 }
 
 // Everything the kernels need for one (m, k, n, p, u, v) problem.
+enum Engine { kDmma = 0, kI8 = 1 };
+
 struct Job {
   i64 m, k, n;
   u64 p;
   int u, v;
+  int engine = kDmma;
+  int D = 0;  // int8 engine: base-256 digits per residue
   int BM = 0, BN = 0, MB = 0, NB = 0, KB = 0;
-  size_t apack_elems = 0, bpack_elems = 0;
+  size_t apack_bytes = 0, bpack_bytes = 0, per_rb_bytes = 0;
   i64 lambda_k = 0;
   GemmParams gp{};
   DigitParams da{}, db{};
+  i8::Params ip{};
 };
 
-Job make_job(i64 m, i64 k, i64 n, u64 p, int u, int v) {
+template <typename F>
+void dispatch_d(int D, F&& f) {
+  switch (D) {
+    case 1: return f.template operator()<1>();
+    case 2: return f.template operator()<2>();
+    case 3: return f.template operator()<3>();
+    case 4: return f.template operator()<4>();
+    case 5: return f.template operator()<5>();
+    case 6: return f.template operator()<6>();
+    case 7: return f.template operator()<7>();
+  }
+  throw Failure(FPMM_B200_EERROR, "int8 engine: unsupported digit count " + std::to_string(D));
+}
+
+int resolve_engine(unsigned flags) {
+  if (flags & FPMM_B200_ENGINE_I8) return kI8;
+  if (flags & FPMM_B200_ENGINE_DMMA) return kDmma;
+  return kDmma;
+}
+
+Job make_i8_job(i64 m, i64 k, i64 n, u64 p) {
+  Job j;
+  j.m = m, j.k = k, j.n = n, j.p = p, j.engine = kI8;
+  j.D = std::max(1, (bitsize(p - 1) + 7) / 8);
+  j.BM = i8::kBM;
+  j.BN = i8::kBN;
+  j.MB = static_cast<int>((m + i8::kBM - 1) / i8::kBM);
+  j.NB = static_cast<int>((n + i8::kBN - 1) / i8::kBN);
+  j.KB = static_cast<int>((k + i8::kBK - 1) / i8::kBK);
+  dispatch_d(j.D, [&]<int D>() {
+    j.per_rb_bytes = static_cast<size_t>(j.KB) * i8::Cfg<D>::kAStage;
+    j.apack_bytes = static_cast<size_t>(j.MB) * j.per_rb_bytes;
+    j.bpack_bytes = static_cast<size_t>(j.NB) * j.KB * i8::Cfg<D>::kBStage;
+  });
+  // exact while pairs * K_seg * 255^2 < 2^32 (weight block read as unsigned)
+  const u64 terms = 0xFFFFFFFFull / (static_cast<u64>(j.D) * 255 * 255);
+  const i64 seg_kb = std::max<i64>(1, static_cast<i64>(terms) / i8::kBK);
+  j.lambda_k = seg_kb * i8::kBK;
+  i8::Params& q = j.ip;
+  q.m = m, q.n = n, q.MB = j.MB, q.NB = j.NB, q.KB = j.KB;
+  q.seg_kb = static_cast<int>(std::min<i64>(seg_kb, j.KB > 0 ? j.KB : 1));
+  q.p = p;
+  q.mu = static_cast<unsigned long long>((static_cast<u128>(1) << 64) / p);
+  return j;
+}
+
+Job make_job(i64 m, i64 k, i64 n, u64 p, int u, int v, int engine = kDmma) {
+  if (engine == kI8) {
+    Job j = make_i8_job(m, k, n, p);
+    j.u = u, j.v = v;
+    return j;
+  }
   Job j;
   j.m = m, j.k = k, j.n = n, j.p = p, j.u = u, j.v = v;
   dispatch(u, v, [&]<int U, int V, int MT, int NT>() {
@@ -157,8 +225,9 @@ Job make_job(i64 m, i64 k, i64 n, u64 p, int u, int v) {
     j.MB = static_cast<int>((m + Cfg::BM - 1) / Cfg::BM);
     j.NB = static_cast<int>((n + Cfg::BN - 1) / Cfg::BN);
     j.KB = static_cast<int>((k + 15) / 16);
-    j.apack_elems = static_cast<size_t>(j.MB) * j.KB * Cfg::kAElems;
-    j.bpack_elems = static_cast<size_t>(j.NB) * j.KB * Cfg::kBElems;
+    j.per_rb_bytes = static_cast<size_t>(j.KB) * Cfg::kAElems * sizeof(double);
+    j.apack_bytes = static_cast<size_t>(j.MB) * j.per_rb_bytes;
+    j.bpack_bytes = static_cast<size_t>(j.NB) * j.KB * Cfg::kBElems * sizeof(double);
   });
   j.lambda_k = kernel_block(p, u, v, 4);
   if (j.lambda_k < 4)
@@ -184,32 +253,84 @@ Job make_job(i64 m, i64 k, i64 n, u64 p, int u, int v) {
   return j;
 }
 
-void launch_pack_a(const Job& j, const double* A, i64 lda, i64 rows, double* apack, int* err,
+void launch_pack_a(const Job& j, const double* A, i64 lda, i64 rows, void* apack, int* err,
                    cudaStream_t s) {
+  if (j.engine == kI8) {
+    if (err && rows > 0 && j.k > 0)
+      check_residues_kernel<<<grid_for(rows * j.k, 256), 256, 0, s>>>(A, lda, rows, j.k, j.p, err);
+    const i64 mpad = ((rows + i8::kBM - 1) / i8::kBM) * i8::kBM;
+    const i64 items = mpad * j.KB * (i8::kBK / 16);
+    dispatch_d(j.D, [&]<int D>() {
+      i8::pack_a_i8<D><<<grid_for(items, 256), 256, 0, s>>>(A, lda, rows, j.k, j.KB, mpad,
+                                                            static_cast<uint8_t*>(apack));
+    });
+    CUDA_OK(cudaGetLastError());
+    return;
+  }
   dispatch(j.u, j.v, [&]<int U, int V, int MT, int NT>() {
     using Cfg = GemmCfg<U, V, MT, NT>;
     const i64 mb = (rows + Cfg::BM - 1) / Cfg::BM;
     const i64 mpad = mb * Cfg::BM;
     const i64 items = (mpad / 2) * j.KB * 16;
     pack_a_kernel<U, Cfg::BM><<<grid_for(items, 256), 256, 0, s>>>(A, lda, rows, j.k, j.KB, mpad, j.da,
-                                                                   apack, err);
+                                                                   static_cast<double*>(apack), err);
   });
   CUDA_OK(cudaGetLastError());
 }
 
-void launch_pack_b(const Job& j, const double* B, i64 ldb, double* bpack, int* err, cudaStream_t s) {
+void launch_pack_b(const Job& j, const double* B, i64 ldb, void* bpack, int* err, cudaStream_t s) {
+  if (j.engine == kI8) {
+    if (err && j.k > 0 && j.n > 0)
+      check_residues_kernel<<<grid_for(j.k * j.n, 256), 256, 0, s>>>(B, ldb, j.k, j.n, j.p, err);
+    const i64 tiles = static_cast<i64>(j.KB) * j.NB;
+    dispatch_d(j.D, [&]<int D>() {
+      i8::pack_b_i8<D><<<static_cast<unsigned>(std::min<i64>(std::max<i64>(tiles, 1), 148 * 16)), 256, 0, s>>>(
+          B, ldb, j.k, j.n, j.KB, j.NB, static_cast<uint8_t*>(bpack));
+    });
+    CUDA_OK(cudaGetLastError());
+    return;
+  }
   dispatch(j.u, j.v, [&]<int U, int V, int MT, int NT>() {
     using Cfg = GemmCfg<U, V, MT, NT>;
     const i64 npad = static_cast<i64>(j.NB) * Cfg::BN;
     const i64 items = (npad / 2) * j.KB * 16;
     pack_b_kernel<V, Cfg::BN><<<grid_for(items, 256), 256, 0, s>>>(B, ldb, j.k, j.n, j.KB, npad, j.db,
-                                                                   bpack, err);
+                                                                   static_cast<double*>(bpack), err);
   });
   CUDA_OK(cudaGetLastError());
 }
 
-void launch_gemm(const Job& j, const double* apack, const double* bpack, double* C, i64 ldc, i64 rows,
+void launch_gemm_i8(const Job& j, const void* apack, const void* bpack, double* C, i64 ldc, i64 rows,
+                    cudaStream_t s) {
+  i8::Params q = j.ip;
+  q.apack = static_cast<const uint8_t*>(apack);
+  q.bpack = static_cast<const uint8_t*>(bpack);
+  q.C = C;
+  q.ldc = ldc;
+  q.m = rows;
+  q.MB = static_cast<int>((rows + i8::kBM - 1) / i8::kBM);
+  dispatch_d(j.D, [&]<int D>() {
+    using CF = i8::Cfg<D>;
+    auto kern = i8::mwi8_kernel<D>;
+    static bool configured[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!configured[dev & 63]) {
+      CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::kSmem));
+      configured[dev & 63] = true;
+    }
+    const i64 tiles = static_cast<i64>(q.MB) * q.NB;
+    if (tiles > 0x7fffffff) throw Failure(FPMM_B200_EERROR, "problem too large for one launch");
+    kern<<<static_cast<unsigned>(tiles), i8::kThreads, CF::kSmem, s>>>(q);
+  });
+  CUDA_OK(cudaGetLastError());
+}
+
+void launch_gemm(const Job& j, const void* apack_v, const void* bpack_v, double* C, i64 ldc, i64 rows,
                  cudaStream_t s) {
+  if (j.engine == kI8) return launch_gemm_i8(j, apack_v, bpack_v, C, ldc, rows, s);
+  const double* apack = static_cast<const double*>(apack_v);
+  const double* bpack = static_cast<const double*>(bpack_v);
   GemmParams g = j.gp;
   g.apack = apack;
   g.bpack = bpack;
@@ -289,9 +410,9 @@ void product_device(const ProductArgs& a, int device, void* stream, fpmm_b200_ti
     if (!(a.flags & FPMM_B200_ASYNC)) CUDA_OK(cudaStreamSynchronize(s));
     return;
   }
-  const Job j = make_job(a.m, a.k, a.n, a.p, a.u, a.v);
-  double* apack = static_cast<double*>(c.apack.get(j.apack_elems * sizeof(double)));
-  double* bpack = static_cast<double*>(c.bpack.get(j.bpack_elems * sizeof(double)));
+  const Job j = make_job(a.m, a.k, a.n, a.p, a.u, a.v, resolve_engine(a.flags));
+  void* apack = c.apack.get(j.apack_bytes);
+  void* bpack = c.bpack.get(j.bpack_bytes);
   int* err = nullptr;
   if (a.flags & FPMM_B200_CHECK_INPUTS) {
     err = static_cast<int*>(c.err.get(sizeof(int)));
@@ -359,43 +480,66 @@ void product_host(const ProductArgs& a, int ngpus, fpmm_b200_timing* tm) {
     for (i64 r = 0; r < a.m; ++r) std::memset(a.C + r * a.ldc, 0, sizeof(double) * a.n);
     return;
   }
-  const Job j = make_job(a.m, a.k, a.n, a.p, a.u, a.v);
+  const Job j = make_job(a.m, a.k, a.n, a.p, a.u, a.v, resolve_engine(a.flags));
   const unsigned chk = a.flags & FPMM_B200_CHECK_INPUTS;
 
   if (ngpus == 1) {
+    // Three-stream pipeline over row chunks of A / C: H2D of chunk i+1 and
+    // D2H of chunk i-1 overlap the fused kernel on chunk i (PCIe is full
+    // duplex); B goes first since every chunk needs its words.
     DeviceCtx& c = ctx(0);
-    cudaStream_t s = c.stream;
+    cudaStream_t s = c.stream, si = c.s_in, so = c.s_out;
     double* dA = static_cast<double*>(c.a.get(sizeof(double) * a.m * a.k));
     double* dB = static_cast<double*>(c.b.get(sizeof(double) * a.k * a.n));
     double* dC = static_cast<double*>(c.c.get(sizeof(double) * a.m * a.n));
-    double* apack = static_cast<double*>(c.apack.get(j.apack_elems * sizeof(double)));
-    double* bpack = static_cast<double*>(c.bpack.get(j.bpack_elems * sizeof(double)));
+    uint8_t* apack = static_cast<uint8_t*>(c.apack.get(j.apack_bytes));
+    void* bpack = c.bpack.get(j.bpack_bytes);
+    const size_t per_rb = j.per_rb_bytes;
+    // ~8 chunks of whole GEMM row tiles once the operands are large enough to matter
+    const i64 bytes = 8 * (a.m * a.k + a.m * a.n);
+    const int want = bytes >= (i64{64} << 20) ? DeviceCtx::kChunks : 1;
+    const i64 tiles = (a.m + j.BM - 1) / j.BM;
+    const i64 chunk_rows = ((tiles + want - 1) / want) * j.BM;
+    const int nch = static_cast<int>((a.m + chunk_rows - 1) / chunk_rows);
     int* err = nullptr;
     if (chk) {
       err = static_cast<int*>(c.err.get(sizeof(int)));
       CUDA_OK(cudaMemsetAsync(err, 0, sizeof(int), s));
+      CUDA_OK(cudaStreamSynchronize(s));
     }
-    CUDA_OK(cudaEventRecord(c.ev[0], s));
-    CUDA_OK(cudaMemcpy2DAsync(dA, a.k * 8, a.A, a.lda * 8, a.k * 8, a.m, cudaMemcpyHostToDevice, s));
-    CUDA_OK(cudaMemcpy2DAsync(dB, a.n * 8, a.B, a.ldb * 8, a.n * 8, a.k, cudaMemcpyHostToDevice, s));
-    CUDA_OK(cudaEventRecord(c.ev[1], s));
-    launch_pack_a(j, dA, a.k, a.m, apack, err, s);
-    launch_pack_b(j, dB, a.n, bpack, err, s);
+    CUDA_OK(cudaEventRecord(c.ev[0], si));
+    CUDA_OK(cudaMemcpy2DAsync(dB, a.n * 8, a.B, a.ldb * 8, a.n * 8, a.k, cudaMemcpyHostToDevice, si));
+    CUDA_OK(cudaEventRecord(c.ev[1], si));
+    for (int i = 0; i < nch; ++i) {
+      const i64 r0 = i * chunk_rows, rn = std::min<i64>(a.m - r0, chunk_rows);
+      CUDA_OK(cudaMemcpy2DAsync(dA + r0 * a.k, a.k * 8, a.A + r0 * a.lda, a.lda * 8, a.k * 8, rn,
+                                cudaMemcpyHostToDevice, si));
+      CUDA_OK(cudaEventRecord(c.ev_in[i], si));
+    }
+    CUDA_OK(cudaStreamWaitEvent(s, c.ev[1], 0));
     CUDA_OK(cudaEventRecord(c.ev[2], s));
-    launch_gemm(j, apack, bpack, dC, a.n, a.m, s);
-    CUDA_OK(cudaEventRecord(c.ev[3], s));
-    CUDA_OK(cudaMemcpy2DAsync(a.C, a.ldc * 8, dC, a.n * 8, a.n * 8, a.m, cudaMemcpyDeviceToHost, s));
-    CUDA_OK(cudaEventRecord(c.ev[4], s));
-    CUDA_OK(cudaStreamSynchronize(s));
+    launch_pack_b(j, dB, a.n, bpack, err, s);
+    for (int i = 0; i < nch; ++i) {
+      const i64 r0 = i * chunk_rows, rn = std::min<i64>(a.m - r0, chunk_rows);
+      uint8_t* ap = apack + static_cast<size_t>(r0 / j.BM) * per_rb;
+      CUDA_OK(cudaStreamWaitEvent(s, c.ev_in[i], 0));
+      launch_pack_a(j, dA + r0 * a.k, a.k, rn, ap, err, s);
+      launch_gemm(j, ap, bpack, dC + r0 * a.n, a.n, rn, s);
+      CUDA_OK(cudaEventRecord(c.ev_out[i], s));
+      CUDA_OK(cudaStreamWaitEvent(so, c.ev_out[i], 0));
+      CUDA_OK(cudaMemcpy2DAsync(a.C + r0 * a.ldc, a.ldc * 8, dC + r0 * a.n, a.n * 8, a.n * 8, rn,
+                                cudaMemcpyDeviceToHost, so));
+    }
+    CUDA_OK(cudaEventRecord(c.ev[3], so));
+    CUDA_OK(cudaStreamSynchronize(so));
     if (err) check_err_flag(c, s);
     if (tm) {
-      tm->h2d_ms = elapsed(c.ev[0], c.ev[1]);
-      tm->pack_ms = elapsed(c.ev[1], c.ev[2]);
-      tm->gemm_ms = elapsed(c.ev[2], c.ev[3]);
-      tm->d2h_ms = elapsed(c.ev[3], c.ev[4]);
-      tm->total_ms = elapsed(c.ev[0], c.ev[4]);
+      tm->h2d_ms = elapsed(c.ev[0], c.ev_in[nch - 1]);
+      tm->gemm_ms = elapsed(c.ev[2], c.ev_out[nch - 1]);  // pack + fused GEMM span (overlaps copies)
+      tm->d2h_ms = elapsed(c.ev_out[nch - 1], c.ev[3]);  // exposed tail of the D2H
+      tm->total_ms = elapsed(c.ev[0], c.ev[3]);
       tm->lambda_k = j.lambda_k;
-      tm->launches = 3;
+      tm->launches = 1 + 2 * nch;
       tm->ngpus = 1;
     }
     return;
@@ -413,7 +557,8 @@ void product_host(const ProductArgs& a, int ngpus, fpmm_b200_timing* tm) {
   }
   std::vector<DeviceCtx*> cs(ngpus);
   for (int g = 0; g < ngpus; ++g) cs[g] = &ctx(g);
-  std::vector<double*> dA(ngpus), dC(ngpus), apack(ngpus), bpack(ngpus);
+  std::vector<double*> dA(ngpus), dC(ngpus);
+  std::vector<void*> apack(ngpus), bpack(ngpus);
   std::vector<int*> errs(ngpus, nullptr);
   double* dB0 = nullptr;
   for (int g = 0; g < ngpus; ++g) {
@@ -421,8 +566,8 @@ void product_host(const ProductArgs& a, int ngpus, fpmm_b200_timing* tm) {
     CUDA_OK(cudaSetDevice(g));
     dA[g] = static_cast<double*>(c.a.get(sizeof(double) * std::max<i64>(rn[g], 1) * a.k));
     dC[g] = static_cast<double*>(c.c.get(sizeof(double) * std::max<i64>(rn[g], 1) * a.n));
-    apack[g] = static_cast<double*>(c.apack.get(j.apack_elems * sizeof(double)));
-    bpack[g] = static_cast<double*>(c.bpack.get(j.bpack_elems * sizeof(double)));
+    apack[g] = c.apack.get(j.apack_bytes);
+    bpack[g] = c.bpack.get(j.bpack_bytes);
     if (chk) {
       errs[g] = static_cast<int*>(c.err.get(sizeof(int)));
       CUDA_OK(cudaMemsetAsync(errs[g], 0, sizeof(int), c.stream));
@@ -443,7 +588,7 @@ void product_host(const ProductArgs& a, int ngpus, fpmm_b200_timing* tm) {
   NCCL_OK(nccl().GroupStart());
   for (int g = 0; g < ngpus; ++g) {
     CUDA_OK(cudaSetDevice(g));
-    NCCL_OK(nccl().Broadcast(bpack[0], bpack[g], j.bpack_elems, ncclDouble, 0, g_all.comms[g], cs[g]->stream));
+    NCCL_OK(nccl().Broadcast(bpack[0], bpack[g], j.bpack_bytes, ncclUint8, 0, g_all.comms[g], cs[g]->stream));
   }
   NCCL_OK(nccl().GroupEnd());
   for (int g = 0; g < ngpus; ++g) {
@@ -680,9 +825,10 @@ void dist_finalize() {
 
 void dist_rows(i64 m, int nranks, int rank, int u, int v, i64* row0, i64* rows) {
   if (nranks < 1 || rank < 0 || rank >= nranks) throw Failure(FPMM_B200_EERROR, "dist_rows: bad rank/size");
-  int bm = 64;
-  dispatch(u, v, [&]<int U, int V, int MT, int NT>() { bm = GemmCfg<U, V, MT, NT>::BM; });
-  const i64 per = part_rows(m, nranks, bm);
+  // 128 = a multiple of every engine's CTA row tile (DMMA BM in {32,64,128},
+  // int8 BM = 128), so each rank packs whole tiles whatever the engine
+  dispatch(u, v, [&]<int U, int V, int MT, int NT>() {});  // rejects unsupported (u,v)
+  const i64 per = part_rows(m, nranks, 128);
   const i64 r0 = std::min<i64>(m, rank * per);
   *row0 = r0;
   *rows = std::min<i64>(m, r0 + per) - r0;
@@ -703,11 +849,11 @@ void dist_product_device(const double* dA_rows, i64 lda, const double* dB, i64 l
   }
   DeviceCtx& c = ctx(g_dist.device);
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c.stream;
-  const Job j = make_job(m, k, n, p, u, v);
+  const Job j = make_job(m, k, n, p, u, v, resolve_engine(flags));
   i64 r0 = 0, rn = 0;
   dist_rows(m, g_dist.nranks, g_dist.rank, u, v, &r0, &rn);
-  double* apack = static_cast<double*>(c.apack.get(j.apack_elems * sizeof(double)));
-  double* bpack = static_cast<double*>(c.bpack.get(j.bpack_elems * sizeof(double)));
+  void* apack = c.apack.get(j.apack_bytes);
+  void* bpack = c.bpack.get(j.bpack_bytes);
   int* err = nullptr;
   if (flags & FPMM_B200_CHECK_INPUTS) {
     err = static_cast<int*>(c.err.get(sizeof(int)));
@@ -717,7 +863,7 @@ void dist_product_device(const double* dA_rows, i64 lda, const double* dB, i64 l
   if (g_dist.rank == root) launch_pack_b(j, dB, ldb, bpack, err, s);
   if (rn > 0) launch_pack_a(j, dA_rows, lda, rn, apack, err, s);
   CUDA_OK(cudaEventRecord(c.ev[1], s));
-  NCCL_OK(nccl().Broadcast(bpack, bpack, j.bpack_elems, ncclDouble, root, g_dist.comm, s));
+  NCCL_OK(nccl().Broadcast(bpack, bpack, j.bpack_bytes, ncclUint8, root, g_dist.comm, s));
   CUDA_OK(cudaEventRecord(c.ev[2], s));
   if (rn > 0) launch_gemm(j, apack, bpack, dC_rows, ldc, rn, s);
   CUDA_OK(cudaEventRecord(c.ev[3], s));

@@ -1,0 +1,363 @@
+// i8engine.cuh -- int8 multiword engine on the 5th-gen tensor cores (tcgen05).
+//
+// The same multiword method with 8-bit words: every residue x < p < 2^(8D) is
+// split into D unsigned base-256 digits, x = sum_i 256^i x_i.  Then
+//   A B = sum_s 256^s T_s,   T_s = sum_{i+j=s} A_i B_j   (s = 0 .. 2D-2)
+// and each T_s is an exact integer sum of digit products (<= 255^2 each)
+// computed by tcgen05.mma.kind::i8 into int32 TMEM accumulators.  Read as
+// unsigned, a T_s block is exact while pairs(s) * Kseg * 255^2 < 2^32, so K is
+// processed in segments of at most Kseg; the epilogue folds the 2D-1 blocks
+// with Horner's rule mod p (Barrett) and accumulates the segments.
+//
+// One CTA computes a 128 x 32 tile of C.  B's digits are concatenated along
+// N (B_cat = [B_0 | .. | B_{D-1}], N_mma = 32 D) and the MMA of A digit i is
+// issued at TMEM column offset 32 i, so digit pair (i, j) lands in column
+// block i + j = s: one MMA per A digit per k-step builds every T_s at once,
+// in (2D-1) * 32 <= 416 TMEM columns.
+//
+// Warp roles: warp 0 TMA producer (1-D bulk copies of pre-packed chunks),
+// warp 1 TMEM allocator + single-thread MMA issuer, warps 2-5 epilogue
+// (TMEM -> registers -> mod-p fold -> C).
+#pragma once
+
+#include <cstdint>
+
+#include "device_common.cuh"
+
+namespace fpmm_b200 {
+namespace i8 {
+
+using i64 = std::int64_t;
+
+constexpr int kBM = 128;      // rows per CTA tile (MMA M)
+constexpr int kBN = 32;       // output columns per CTA tile
+constexpr int kBK = 64;       // k bytes (int8 elements) per pipeline stage
+constexpr int kKSteps = kBK / 32;  // MMA K = 32 for kind::i8
+constexpr int kThreads = 192;      // 6 warps
+
+template <int D>
+struct Cfg {
+  static constexpr int kAStage = D * kBM * kBK;        // bytes: D digit tiles of 128 x 64
+  static constexpr int kBStage = D * kBN * kBK;        // bytes: B_cat tile of (32 D) x 64
+  static constexpr int kStageBytes = kAStage + kBStage;
+  static constexpr int kStages = (220 * 1024) / kStageBytes > 8 ? 8 : (220 * 1024) / kStageBytes;
+  static constexpr int kBlocks = 2 * D - 1;            // weight blocks s = 0 .. 2D-2
+  static constexpr int kTmemCols = kBlocks * kBN;
+  static constexpr int kTmemAlloc = kTmemCols <= 32 ? 32 : kTmemCols <= 64 ? 64 : kTmemCols <= 128 ? 128
+                                    : kTmemCols <= 256 ? 256 : 512;
+  static constexpr int kSmem = kStages * kStageBytes + 1024;  // + barriers / tmem slot
+  static constexpr int kNmma = D * kBN;
+  static_assert(kStages >= 2, "pipeline needs two stages");
+};
+
+// ------------------------------------------------------------ descriptors
+// UMMA shared-memory descriptor, K-major, no swizzle (canonical
+// ((8,n),2):((16B,SBO),LBO)): 8-row x 16-byte core matrices, LBO = byte step
+// between the two 16-byte K halves of one MMA, SBO = byte step between
+// 8-row groups.  Version 1 (sm_100), layout type 0.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+  d |= static_cast<uint64_t>(1) << 46;  // version
+  return d;
+}
+
+// Instruction descriptor: kind::i8, D = S32, A = B = unsigned 8-bit, both
+// K-major, N >> 3 at bit 17, M >> 4 at bit 24.
+__host__ __device__ constexpr uint32_t instr_desc(int M, int N) {
+  return (2u << 4) | (0u << 7) | (0u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
+         (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  const uint32_t z = 0;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %5, %5, %5}, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(z));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                   dev::smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_st32_zero(uint32_t taddr) {
+  const uint32_t z = 0;
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+      "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};\n" ::"r"(taddr),
+      "r"(z)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+
+// x mod p for x < 2^64 with mu = floor(2^64 / p): q = mulhi(x, mu) is floor(x/p)
+// or one less, so a single correction lands in [0, p).
+__device__ __forceinline__ uint64_t barrett(uint64_t x, uint64_t p, uint64_t mu) {
+  const uint64_t q = __umul64hi(x, mu);
+  uint64_t r = x - q * p;
+  return r >= p ? r - p : r;
+}
+
+struct Params {
+  const uint8_t* apack;  // [m-block][k-block] chunks of kAStage bytes
+  const uint8_t* bpack;  // [n-block][k-block] chunks of kBStage bytes
+  double* C;
+  i64 ldc, m, n;
+  int MB, NB, KB;       // tiles along m, n and 64-byte k-blocks
+  int seg_kb;           // k-blocks per exact accumulation segment
+  unsigned long long p, mu;
+};
+
+// --------------------------------------------------------------- packing
+// A: m x k residues -> D unsigned digit planes in the MMA's canonical
+// K-major layout.  Chunk (rb, kb) (contiguous, kAStage bytes):
+//   [digit i][k16 c (4)][row group g (16)][row r (8)][16 bytes]
+// Thread (row, 16-byte k chunk): reads 16 residues, writes D x 16 bytes.
+template <int D>
+__global__ void __launch_bounds__(256) pack_a_i8(const double* __restrict__ A, i64 lda, i64 m, i64 k,
+                                                 int KB, i64 mpad, uint8_t* __restrict__ out) {
+  const i64 kchunks = static_cast<i64>(KB) * (kBK / 16);
+  const i64 total = mpad * kchunks;
+  for (i64 idx = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += static_cast<i64>(gridDim.x) * blockDim.x) {
+    // warp covers 8 rows x 4 chunks so each 128-byte core matrix line is written whole
+    const i64 grp = idx / 32;
+    const int lane = static_cast<int>(idx % 32);
+    const int r8 = lane % 8, c4 = lane / 8;
+    const i64 rows8 = mpad / 8;
+    const i64 rg = grp % rows8, cq = grp / rows8;  // row group of 8, chunk quad
+    const i64 row = rg * 8 + r8;
+    const i64 kc = cq * 4 + c4;  // 16-byte chunk index along k
+    if (kc >= kchunks) continue;
+    uint32_t w[D][4];
+#pragma unroll
+    for (int i = 0; i < D; ++i) w[i][0] = w[i][1] = w[i][2] = w[i][3] = 0;
+    if (row < m) {
+      const double* src = A + row * lda + kc * 16;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const i64 col = kc * 16 + e;
+        const unsigned long long x = col < k ? static_cast<unsigned long long>(src[e]) : 0ull;
+#pragma unroll
+        for (int i = 0; i < D; ++i) w[i][e / 4] |= static_cast<uint32_t>((x >> (8 * i)) & 0xFF) << (8 * (e % 4));
+      }
+    }
+    const i64 rb = row / kBM, kb = kc / (kBK / 16);
+    const int c = static_cast<int>(kc % (kBK / 16)), g = static_cast<int>((row % kBM) / 8);
+    uint8_t* base = out + (rb * KB + kb) * static_cast<i64>(Cfg<D>::kAStage);
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+      *reinterpret_cast<uint4*>(base + i * (kBM * kBK) + ((c * (kBM / 8) + g) * 8 + r8) * 16) =
+          make_uint4(w[i][0], w[i][1], w[i][2], w[i][3]);
+  }
+}
+
+// B: k x n residues -> B_cat digit rows (digit j, column c) -> row 32 j + c,
+// K-major.  Chunk (cb, kb) (contiguous, kBStage bytes):
+//   [k16 c (4)][row group g (4 D)][row r (8)][16 bytes]
+// A block transposes a 64 (k) x 32 (col) tile through shared memory.
+template <int D>
+__global__ void __launch_bounds__(256) pack_b_i8(const double* __restrict__ B, i64 ldb, i64 k, i64 n,
+                                                 int KB, int NB, uint8_t* __restrict__ out) {
+  __shared__ unsigned long long tile[kBK][kBN + 1];
+  const i64 tiles = static_cast<i64>(KB) * NB;
+  for (i64 t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const i64 cb = t % NB, kb = t / NB;
+    __syncthreads();
+    for (int e = threadIdx.x; e < kBK * kBN; e += blockDim.x) {
+      const int kr = e / kBN, cc = e % kBN;
+      const i64 kk = kb * kBK + kr, col = cb * kBN + cc;
+      tile[kr][cc] = (kk < k && col < n) ? static_cast<unsigned long long>(B[kk * ldb + col]) : 0ull;
+    }
+    __syncthreads();
+    uint8_t* base = out + (cb * KB + kb) * static_cast<i64>(Cfg<D>::kBStage);
+    // units: (digit j, column c, k16 chunk q): 16 bytes each
+    for (int u = threadIdx.x; u < D * kBN * (kBK / 16); u += blockDim.x) {
+      const int q = u % (kBK / 16), cc = (u / (kBK / 16)) % kBN, j = u / ((kBK / 16) * kBN);
+      uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int e = 0; e < 16; ++e)
+        w[e / 4] |= static_cast<uint32_t>((tile[q * 16 + e][cc] >> (8 * j)) & 0xFF) << (8 * (e % 4));
+      const int nn = j * kBN + cc, g = nn / 8, r8 = nn % 8;
+      *reinterpret_cast<uint4*>(base + ((q * (D * kBN / 8) + g) * 8 + r8) * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ GEMM
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1) mwi8_kernel(const __grid_constant__ Params P) {
+  using CF = Cfg<D>;
+  constexpr int S = CF::kStages;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S * CF::kAStage;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * CF::kStageBytes);
+  uint64_t* empty = full + S;
+  uint64_t* tmem_full = empty + S;
+  uint64_t* tmem_empty = tmem_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int tm = blockIdx.x / P.NB, tn = blockIdx.x % P.NB;  // consecutive CTAs share the A panel
+  const int nseg = (P.KB + P.seg_kb - 1) / P.seg_kb;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      dev::mbar_init(&full[s], 1);
+      dev::mbar_init(&empty[s], 1);
+    }
+    dev::mbar_init(tmem_full, 1);
+    dev::mbar_init(tmem_empty, 4);  // one arrive per epilogue warp
+    dev::fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     dev::smem_u32(tmem_slot)),
+                 "r"(CF::kTmemAlloc));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      const uint8_t* gA = P.apack + static_cast<i64>(tm) * P.KB * CF::kAStage;
+      const uint8_t* gB = P.bpack + static_cast<i64>(tn) * P.KB * CF::kBStage;
+      for (int kb = 0; kb < P.KB; ++kb) {
+        const int s = kb % S;
+        if (kb >= S) dev::mbar_wait(&empty[s], ((kb / S) - 1) & 1);
+        dev::mbar_arrive_expect_tx(&full[s], CF::kStageBytes);
+        dev::bulk_g2s(sA + s * CF::kAStage, gA + static_cast<i64>(kb) * CF::kAStage, CF::kAStage, &full[s]);
+        dev::bulk_g2s(sB + s * CF::kBStage, gB + static_cast<i64>(kb) * CF::kBStage, CF::kBStage, &full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (one thread) ----------------
+    if (lane == 0) {
+      constexpr uint32_t idesc = instr_desc(kBM, CF::kNmma);
+      int kb = 0;
+      for (int seg = 0; seg < nseg; ++seg) {
+        dev::mbar_wait(tmem_empty, seg & 1);  // epilogue zeroed / drained the accumulators
+        fence_after();
+        const int kend = min(P.KB, kb + P.seg_kb);
+        for (; kb < kend; ++kb) {
+          const int s = kb % S;
+          dev::mbar_wait(&full[s], (kb / S) & 1);
+          fence_after();
+          const uint32_t a0 = dev::smem_u32(sA + s * CF::kAStage), b0 = dev::smem_u32(sB + s * CF::kBStage);
+#pragma unroll
+          for (int t = 0; t < kKSteps; ++t) {
+            const uint64_t bd = smem_desc(b0 + t * 2 * (CF::kNmma / 8) * 128, (CF::kNmma / 8) * 128, 128);
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+              const uint64_t ad = smem_desc(a0 + i * (kBM * kBK) + t * 2 * (kBM / 8) * 128, (kBM / 8) * 128, 128);
+              mma_i8(tbase + i * kBN, ad, bd, idesc, 1u);
+            }
+          }
+          mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
+        }
+        mma_commit(tmem_full);    // segment accumulators complete
+      }
+    }
+  } else {
+    // ---------------- epilogue: warps 2..5 ----------------
+    const int quad = warp % 4;                 // TMEM lane quadrant this warp may access
+    const int row_in_tile = quad * 32 + lane;  // TMEM lane == tile row
+    const uint32_t trow = tbase + (static_cast<uint32_t>(quad * 32) << 16);
+    const unsigned long long p = P.p, mu = P.mu;
+    unsigned long long res[kBN];
+#pragma unroll
+    for (int c = 0; c < kBN; ++c) res[c] = 0;
+    // zero the accumulators for the first segment
+#pragma unroll
+    for (int b = 0; b < CF::kBlocks; ++b) tmem_st32_zero(trow + b * kBN);
+    tmem_wait_st();
+    fence_before();
+    __syncwarp();
+    if (lane == 0) dev::mbar_arrive(tmem_empty);
+    for (int seg = 0; seg < nseg; ++seg) {
+      dev::mbar_wait(tmem_full, seg & 1);
+      fence_after();
+      unsigned long long h[kBN];
+      uint32_t v[32];
+      tmem_ld32(trow + (CF::kBlocks - 1) * kBN, v);
+      tmem_wait_ld();
+#pragma unroll
+      for (int c = 0; c < kBN; ++c) h[c] = v[c] % p;
+#pragma unroll 1
+      for (int b = CF::kBlocks - 2; b >= 0; --b) {
+        tmem_ld32(trow + b * kBN, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < kBN; ++c) h[c] = barrett((h[c] << 8) + v[c], p, mu);
+      }
+#pragma unroll
+      for (int c = 0; c < kBN; ++c) {
+        const unsigned long long t = res[c] + h[c];
+        res[c] = t >= p ? t - p : t;
+      }
+      if (seg + 1 < nseg) {  // re-zero and hand the accumulators back to the MMA warp
+#pragma unroll
+        for (int b = 0; b < CF::kBlocks; ++b) tmem_st32_zero(trow + b * kBN);
+        tmem_wait_st();
+        fence_before();
+        __syncwarp();
+        if (lane == 0) dev::mbar_arrive(tmem_empty);
+      }
+    }
+    const i64 row = static_cast<i64>(tm) * kBM + row_in_tile;
+    const i64 col0 = static_cast<i64>(tn) * kBN;
+    if (row < P.m) {
+      double* dst = P.C + row * P.ldc + col0;
+      if (col0 + kBN <= P.n && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+#pragma unroll
+        for (int c = 0; c < kBN; c += 2)
+          *reinterpret_cast<double2*>(dst + c) = make_double2(static_cast<double>(res[c]), static_cast<double>(res[c + 1]));
+      } else {
+        for (int c = 0; c < kBN && col0 + c < P.n; ++c) dst[c] = static_cast<double>(res[c]);
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tbase), "r"(CF::kTmemAlloc));
+  }
+}
+
+}  // namespace i8
+}  // namespace fpmm_b200

@@ -67,6 +67,14 @@ __device__ __forceinline__ bool is_residue(double v, long long p) {
   return v >= 0.0 && v < static_cast<double>(p) && v == floor(v);
 }
 
+// FPMM_B200_CHECK_INPUTS for engines whose packers do not validate
+__global__ void check_residues_kernel(const double* __restrict__ M, i64 ld, i64 rows, i64 cols,
+                                      unsigned long long p, int* err) {
+  for (i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; e < rows * cols;
+       e += static_cast<i64>(gridDim.x) * blockDim.x)
+    if (!is_residue(M[(e / cols) * ld + e % cols], static_cast<long long>(p))) atomicOr(err, 1);
+}
+
 // (1) A (m x k, lda) -> packed signed words.  Thread: rows r, r+8 of one
 // 16-row group, one column; consecutive threads walk k (coalesced reads).
 template <int W, int BR>
