@@ -173,6 +173,8 @@ def main():
     ap.add_argument("--bits", default="20-52")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--engine", default="i8", choices=["i8", "dmma"],
+                    help="engine timed for `value`/`e2e` (both are recorded per bitsize)")
     args = ap.parse_args()
     m, k, n, wl_bits = WORKLOADS[args.workload]
     bits_list = wl_bits if wl_bits is not None else parse_bits(args.bits)
@@ -221,28 +223,30 @@ def main():
     Crow = torch.empty((max(max(r[1] for r in rows.values()), 1), n), dtype=torch.float64, device=dev)
     torch.cuda.synchronize()
 
-    peak = F.fp64_peak(local)  # measured FP64 tensor-pipe (DMMA) peak, TFLOP/s
+    # measured tensor-pipe peaks of this GPU (MEASURED_PEAKS.json has neither)
+    peaks = {"dmma": F.fp64_peak(local), "i8": F.i8_peak(local)}
+    eng_flags = {"dmma": F.ENGINE_DMMA, "i8": F.ENGINE_I8}
     # one non-default stream carries every product and the timing events
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
-    gemm_ms = {b: [] for b in bits_list}
     launches = [0]
 
-    def step(record=False):
+    def step(engine, record=None):
+        fl = eng_flags[engine] | (0 if record is not None else F.ASYNC)
         for (b, p, u, v, lam, _) in probs:
             tm = F.Timing()
             if world == 1:
-                F.mw_product_device(A[b], B[b], Cbuf, p, u, v, lam, stream=stream,
-                                    flags=F.ASYNC if not record else 0, timing=tm if record else None)
+                F.mw_product_device(A[b], B[b], Cbuf, p, u, v, lam, stream=stream, flags=fl,
+                                    timing=tm if record is not None else None)
                 launches[0] += 3
             else:
                 r0, rn = rows[b]
                 D.mw_product_device(A[b][:rn], B.get(b), Crow[:rn], p, u, v, lam, m, root=0,
-                                    C_full=Cbuf, stream=stream, flags=F.ASYNC if not record else 0,
-                                    timing=tm if record else None)
+                                    C_full=Cbuf, stream=stream, flags=fl,
+                                    timing=tm if record is not None else None)
                 launches[0] += (2 if rn else 0) + (1 if rank == 0 else 0)
-            if record:
-                gemm_ms[b].append(tm.gemm_ms)
+            if record is not None:
+                record[b] = tm.gemm_ms
 
     def barrier():
         if world > 1:
@@ -250,7 +254,7 @@ def main():
         torch.cuda.synchronize()
 
     for _ in range(args.warmup):
-        step()
+        step(args.engine)
     barrier()
     launches[0] = 0
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -258,7 +262,7 @@ def main():
         barrier()
         e0.record(stream)
         for _ in range(args.steps):
-            step()
+            step(args.engine)
         e1.record(stream)
         barrier()
     elapsed_ms = e0.elapsed_time(e1)
@@ -268,33 +272,63 @@ def main():
         elapsed_ms = float(t.item())
     timed_launches = launches[0]
 
-    # one recorded (per-product event-timed) pass for the per-bitsize table and
-    # the GEMM kernel's roofline (library events on the launching stream)
-    step(record=True)
-    torch.cuda.synchronize()
-
     flops_step = sum(2.0 * m * k * n for _ in probs)
     ms_per_step = elapsed_ms / args.steps
     value = flops_step / (ms_per_step * 1e-3) / 1e9
 
-    per_bits = {}
-    fp64_work = gemm_total = 0.0
-    for (b, p, u, v, lam, lk) in probs:
-        g = gemm_ms[b][-1]
-        rn = rows[b][1]
-        work = 2.0 * u * v * rn * k * n
-        fp64_work += work
-        gemm_total += g
-        per_bits[str(b)] = {"u": u, "v": v, "lambda": lam, "lambda_k": lk,
-                            "gemm_ms": round(g, 3),
-                            "eff_gflops": round(2.0 * rn * k * n / (g * 1e-3) / 1e9, 1),
-                            "fp64_frac": round(work / (g * 1e-3) / 1e12 / peak, 4)}
-    achieved = fp64_work / (gemm_total * 1e-3) / 1e12
-
+    # one recorded pass per engine (library CUDA events around the GEMM kernel
+    # on the launching stream): per-bitsize table and each kernel's roofline
+    traffic_db = {}
+    prof = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic_db = json.load(open(prof))
+        except Exception:
+            traffic_db = {}
+    engines = {}
+    for eng in ("i8", "dmma"):
+        rec = {}
+        step(eng, record=rec)
+        torch.cuda.synchronize()
+        per_bits = {}
+        work = gemm_total = 0.0
+        for (b, p, u, v, lam, lk) in probs:
+            g = rec[b]
+            rn = rows[b][1]
+            if eng == "dmma":
+                w = 2.0 * u * v * rn * k * n           # uv-scaled FP64 work
+                extra = {"lambda_k": lk}
+            else:
+                d = max(1, ((p - 1).bit_length() + 7) // 8)
+                w = 2.0 * d * d * rn * k * n           # D^2 int8 word products
+                extra = {"digits": d}
+            work += w
+            gemm_total += g
+            per_bits[str(b)] = dict({"u": u, "v": v, "lambda": lam, "gemm_ms": round(g, 3),
+                                     "eff_gflops": round(2.0 * rn * k * n / (g * 1e-3) / 1e9, 1),
+                                     "tensor_frac": round(w / (g * 1e-3) / 1e12 / peaks[eng], 4)}, **extra)
+        achieved = work / (gemm_total * 1e-3) / 1e12
+        tr = traffic_db.get(eng, {})
+        engines[eng] = {
+            "eff_gflops": round(flops_step / (gemm_total * 1e-3) / 1e9, 1),
+            "roofline": {"bound": "tensor", "achieved": round(achieved, 3), "peak": round(peaks[eng], 3),
+                         "unit": "TFLOP/s", "frac": round(achieved / peaks[eng], 4),
+                         "traffic": tr.get("dram_bytes_per_launch"),
+                         "kernel": ("mwgemm_kernel: DMMA.8x8x4 FP64 tensor pipe; work = 2uv*mnk FP64 flops"
+                                    if eng == "dmma" else
+                                    "mwi8_kernel: tcgen05.mma.kind::i8 (UTCIMMA), TMEM int32; work = 2*D^2*mnk "
+                                    "int8 tensor ops (reported as TFLOP/s = T int8-op/s)"),
+                         "peak_source": ("measured DMMA-only loop on this GPU (MEASURED_PEAKS.json has no FP64 "
+                                         "entry); vendor FP64 tensor 37.2 TF @1965 MHz" if eng == "dmma" else
+                                         "measured back-to-back tcgen05 kind::i8 M128 N256 K32 MMAs on all SMs "
+                                         "(MEASURED_PEAKS.json has no int8 entry); vendor dense int8 4.5 POPS")},
+            "sweep": per_bits}
+    roof = dict(engines[args.engine]["roofline"])
     # end to end through the public host-buffer API (pinned memory), one step
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(F, D, torch, np, probs, A, B, rows, m, k, n, world, rank, part)
+        e2e = run_e2e(F, D, torch, np, probs, A, B, rows, m, k, n, world, rank, part,
+                      eng_flags[args.engine])
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -310,14 +344,6 @@ def main():
             cpu = {"value": None, "unit": "GFLOP/s", "cores": 0, "kind": "reference",
                    "sample": "unavailable: %s" % ex}
 
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(prof):
-        try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
-
     if rank == 0:
         line = {
             "metric": "effective modular GFLOP/s (2mnk/s) over the prime-bitsize sweep",
@@ -330,14 +356,10 @@ def main():
                        "rule": "plan_for_modulus (paper bound, b=2 scan fix)",
                        "parallelism": "row-sharded x%d, NCCL bcast B words + gather C" % world,
                        "l2": "inputs (512 MiB/operand) larger than L2; no flush"},
-            "roofline": {"bound": "tensor", "achieved": round(achieved, 3), "peak": round(peak, 3),
-                         "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "kernel": "mwgemm_kernel (DMMA.8x8x4 FP64 tensor pipe, uv-scaled work 2uv*mnk)",
-                         "peak_source": "measured DMMA-only loop on this GPU (MEASURED_PEAKS.json has no FP64 entry); "
-                                        "vendor FP64 tensor 37.2 TF @1965 MHz",
-                         "fp64_frac_vendor": round(achieved / 37.2, 4)},
-            "fp64_uv_frac": round(achieved / peak, 4),
-            "sweep": per_bits,
+            "engine": args.engine,
+            "roofline": roof,
+            "fp64_uv_frac": engines["dmma"]["roofline"]["frac"],
+            "engines": engines,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gpu_launches": timed_launches,
@@ -349,7 +371,7 @@ def main():
         torch.distributed.destroy_process_group()
 
 
-def run_e2e(F, D, torch, np, probs, A, B, rows, m, k, n, world, rank, part):
+def run_e2e(F, D, torch, np, probs, A, B, rows, m, k, n, world, rank, part, flags):
     """E: the sweep through the host-buffer public API.  Each product's timed
     region covers H2D of its inputs from pinned memory, the product and the
     D2H of C.  Inputs are staged into the pinned buffers outside the timer."""
@@ -366,9 +388,9 @@ def run_e2e(F, D, torch, np, probs, A, B, rows, m, k, n, world, rank, part):
     b, p, u, v, lam, _ = max(probs, key=lambda t: t[2] * t[3])
     r0, rn = rows[b]
     if world == 1:
-        F.mw_product(hA.numpy(), hB.numpy(), u, v, lam, F.FpContext.make(p), out=hC.numpy())
+        F.mw_product(hA.numpy(), hB.numpy(), u, v, lam, F.FpContext.make(p), out=hC.numpy(), flags=flags)
     else:
-        D.mw_product_host(hA[:rn], hB, hC, p, u, v, lam, m, root=0, scratch=scratch)
+        D.mw_product_host(hA[:rn], hB, hC, p, u, v, lam, m, root=0, scratch=scratch, flags=flags)
     for (b, p, u, v, lam, _) in probs:
         r0, rn = rows[b]
         hA[:rn].copy_(A[b][:rn])
@@ -379,9 +401,10 @@ def run_e2e(F, D, torch, np, probs, A, B, rows, m, k, n, world, rank, part):
             torch.distributed.barrier()
         t0 = time.perf_counter()
         if world == 1:
-            F.mw_product(hA.numpy(), hB.numpy(), u, v, lam, F.FpContext.make(p), out=hC.numpy())
+            F.mw_product(hA.numpy(), hB.numpy(), u, v, lam, F.FpContext.make(p), out=hC.numpy(),
+                         flags=flags)
         else:
-            D.mw_product_host(hA[:rn], hB, hC, p, u, v, lam, m, root=0, scratch=scratch)
+            D.mw_product_host(hA[:rn], hB, hC, p, u, v, lam, m, root=0, scratch=scratch, flags=flags)
             torch.distributed.barrier()
         dt = time.perf_counter() - t0
         if world > 1:

@@ -49,7 +49,7 @@ typedef enum {
 /* engine selection (same results, different tensor-core path):
  *   DMMA: the paper's FP64 multiword product on the FP64 tensor pipe (mma.sync .f64)
  *   I8  : base-256 multiword words on tcgen05.mma.kind::i8 (int32 TMEM accumulators)
- * neither flag = the library default (DMMA) */
+ * neither flag = the library default (I8) */
 #define FPMM_B200_ENGINE_DMMA 0x10u
 #define FPMM_B200_ENGINE_I8 0x20u
 
@@ -205,6 +205,9 @@ int fpmm_b200_random_residues_device(double* dM, int64_t ld, int64_t rows, int64
                                      uint64_t p, uint64_t seed, int device, void* stream);
 /* Measured FP64 tensor-pipe peak (TFLOP/s): a DMMA.8x8x4-only loop. */
 int fpmm_b200_fp64_peak(int device, int iters, double* tflops);
+/* Measured int8 tensor-core peak (TOP/s): back-to-back tcgen05.mma.kind::i8
+ * M=128 N=256 K=32 on every SM. */
+int fpmm_b200_i8_peak(int device, int iters, double* tops);
 
 /* release every device workspace, stream and communicator */
 int fpmm_b200_finalize(void);

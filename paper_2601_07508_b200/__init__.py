@@ -73,6 +73,19 @@ ENGINE_DMMA = 0x10  # FP64 multiword on the FP64 tensor pipe (DMMA)
 ENGINE_I8 = 0x20    # base-256 multiword on tcgen05.mma.kind::i8 (TMEM int32 accumulators)
 ASYNC = 0x100
 PLAIN, WORKSPACE, CONCAT = 0, 1, 2
+_ENGINE_MASK = ENGINE_DMMA | ENGINE_I8
+_default_engine_flags = 0
+
+
+def set_default_engine(name: Optional[str]) -> None:
+    """Engine used when a call passes no ENGINE_* flag: "i8", "dmma" or None
+    (the library default, the int8 tcgen05 engine)."""
+    global _default_engine_flags
+    _default_engine_flags = {"i8": ENGINE_I8, "dmma": ENGINE_DMMA, None: 0}[name]
+
+
+def _eng(flags: int) -> int:
+    return flags if flags & _ENGINE_MASK else flags | _default_engine_flags
 
 
 class _Plan(C.Structure):
@@ -149,6 +162,7 @@ def lib():
                                                    C.POINTER(Timing)]),
         "fpmm_b200_random_residues_device": (i32, [vp, i64, i64, i64, i64, u64, u64, i32, vp]),
         "fpmm_b200_fp64_peak": (i32, [i32, i32, C.POINTER(C.c_double)]),
+        "fpmm_b200_i8_peak": (i32, [i32, i32, C.POINTER(C.c_double)]),
         "fpmm_b200_finalize": (i32, []),
     }
     for name, (res, args) in sig.items():
@@ -392,7 +406,7 @@ def _product(A, B, u, v, lam, F, variant, ngpus=1, flags=0, timing=None, out=Non
         flags |= ALLOW_COMPOSITE
     tm = timing if timing is not None else None
     _check(lib().fpmm_b200_mw_product(_ptr(A), _ld(A), _ptr(B), _ld(B), _ptr(Cm), max(n, 1), m, k,
-                                      n, F.p, u, v, lam, variant, ngpus, flags,
+                                      n, F.p, u, v, lam, variant, ngpus, _eng(flags),
                                       C.byref(tm) if tm is not None else None))
     return Cm
 
@@ -433,7 +447,7 @@ def _words_product(da: WordDecomposition, db: WordDecomposition, m, k, n, lam, F
         flags |= ALLOW_COMPOSITE
     _check(lib().fpmm_b200_mw_product_words(
         _ptr(aw), m * k, max(k, 1), da.base, u, _ptr(bw), k * n, max(n, 1), db.base, v, _ptr(Cm),
-        max(n, 1), m, k, n, F.p, lam, variant, flags,
+        max(n, 1), m, k, n, F.p, lam, variant, _eng(flags),
         C.byref(timing) if timing is not None else None))
     return Cm
 
@@ -531,7 +545,7 @@ def mw_product_device(A, B, Cout, p: int, u: int, v: int, lambda_: int, *, varia
     sp = _stream_handle(stream)
     _check(lib().fpmm_b200_mw_product_device(A.data_ptr(), _dev_ld(A), B.data_ptr(), _dev_ld(B),
                                              Cout.data_ptr(), _dev_ld(Cout), m, k, n, p, u, v,
-                                             lambda_, variant, dev, sp, flags,
+                                             lambda_, variant, dev, sp, _eng(flags),
                                              C.byref(timing) if timing is not None else None))
 
 
@@ -560,6 +574,13 @@ def random_residues_device(M, p: int, seed: int, row0: int = 0, stream=None) -> 
     sp = _stream_handle(stream)
     _check(lib().fpmm_b200_random_residues_device(M.data_ptr(), _dev_ld(M), rows, cols, row0, p,
                                                   seed, M.device.index, sp))
+
+
+def i8_peak(device: int = 0, iters: int = 200000) -> float:
+    """Measured int8 tensor-core (tcgen05 kind::i8) peak of `device` in TOP/s."""
+    out = C.c_double()
+    _check(lib().fpmm_b200_i8_peak(device, iters, C.byref(out)))
+    return out.value
 
 
 def fp64_peak(device: int = 0, iters: int = 20000) -> float:

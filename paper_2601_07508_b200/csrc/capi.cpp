@@ -242,6 +242,10 @@ int fpmm_b200_fp64_peak(int device, int iters, double* tflops) {
   return guarded([&] { *tflops = fp64_peak_tflops(device, iters); });
 }
 
+int fpmm_b200_i8_peak(int device, int iters, double* tops) {
+  return guarded([&] { *tops = i8_peak_tops(device, iters); });
+}
+
 int fpmm_b200_finalize(void) {
   return guarded([&] { finalize_all(); });
 }

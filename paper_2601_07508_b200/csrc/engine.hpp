@@ -50,6 +50,7 @@ int device_count();
 void random_residues_device(double* dM, i64 ld, i64 rows, i64 cols, i64 row0, u64 p, u64 seed, int device,
                             void* stream);
 double fp64_peak_tflops(int device, int iters);
+double i8_peak_tops(int device, int iters);
 void finalize_all();
 
 // multi-process partitioner

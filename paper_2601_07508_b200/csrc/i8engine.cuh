@@ -228,7 +228,15 @@ __global__ void __launch_bounds__(kThreads, 1) mwi8_kernel(const __grid_constant
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int tm = blockIdx.x / P.NB, tn = blockIdx.x % P.NB;  // consecutive CTAs share the A panel
+  // grouped rasterisation: a wave of 148 CTAs covers GROUP tile-rows x ~37
+  // tile-columns, so its A panels (GROUP x 7 MB at D=7, K=8192) and B_cat
+  // panels (37 x 1.8 MB) stay resident in the 126 MB L2
+  constexpr int GROUP = 4;
+  const int in_group = GROUP * P.NB;
+  const int first_m = (static_cast<int>(blockIdx.x) / in_group) * GROUP;
+  const int gsz = min(P.MB - first_m, GROUP);
+  const int tm = first_m + (static_cast<int>(blockIdx.x) % in_group) % gsz;
+  const int tn = (static_cast<int>(blockIdx.x) % in_group) / gsz;
   const int nseg = (P.KB + P.seg_kb - 1) / P.seg_kb;
 
   if (threadIdx.x == 0) {
@@ -356,6 +364,48 @@ __global__ void __launch_bounds__(kThreads, 1) mwi8_kernel(const __grid_constant
   if (warp == 1) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tbase), "r"(CF::kTmemAlloc));
+  }
+}
+
+// Tensor-pipe int8 peak probe: one thread per CTA issues `iters` back-to-back
+// M=128 N=256 K=32 kind::i8 MMAs on zero operands (one CTA per SM).
+__global__ void __launch_bounds__(64, 1) i8_peak_kernel(int iters, int* out) {
+  __shared__ __align__(1024) uint8_t ops[kBM * 32 + 256 * 32];
+  __shared__ uint64_t done;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x / 32;
+  for (int e = threadIdx.x; e < static_cast<int>(sizeof(ops)) / 4; e += blockDim.x)
+    reinterpret_cast<uint32_t*>(ops)[e] = 0;
+  if (threadIdx.x == 0) {
+    dev::mbar_init(&done, 1);
+    dev::fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(dev::smem_u32(&slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tbase = slot;
+  if (threadIdx.x == 0) {
+    const uint32_t a = dev::smem_u32(ops), b = a + kBM * 32;
+    const uint64_t ad = smem_desc(a, (kBM / 8) * 128, 128), bd = smem_desc(b, (256 / 8) * 128, 128);
+    constexpr uint32_t idesc = instr_desc(kBM, 256);
+    for (int it = 0; it < iters; ++it) mma_i8(tbase, ad, bd, idesc, it > 0 ? 1u : 0u);
+    mma_commit(&done);
+    dev::mbar_wait(&done, 0);
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    fence_after();
+    uint32_t v[32];
+    tmem_ld32(tbase + (32u << 16), v);  // warp 1 owns TMEM lanes 32..63
+    tmem_wait_ld();
+    if (v[0] == 12345u) out[0] = 1;
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tbase));
   }
 }
 

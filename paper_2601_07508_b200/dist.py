@@ -15,7 +15,7 @@ from __future__ import annotations
 import ctypes as C
 from typing import Optional
 
-from . import Error, Timing, _check, _dev_ld, _stream_handle, lib
+from . import Error, Timing, _check, _dev_ld, _eng, _stream_handle, lib
 
 
 class Partitioner:
@@ -80,11 +80,11 @@ def mw_product_device(A_rows, B, C_rows, p: int, u: int, v: int, lambda_: int, m
     _check(lib().fpmm_b200_dist_mw_product_device(
         A_rows.data_ptr(), max(k, 1) if A_rows.shape[0] <= 1 else _dev_ld(A_rows), bptr, ldb,
         C_rows.data_ptr(), max(n, 1) if C_rows.shape[0] <= 1 else _dev_ld(C_rows), cf, ldcf, m, k, n,
-        p, u, v, lambda_, root, sp, flags, C.byref(timing) if timing is not None else None))
+        p, u, v, lambda_, root, sp, _eng(flags), C.byref(timing) if timing is not None else None))
 
 
 def mw_product_host(A_rows_host, B_host, C_host, p: int, u: int, v: int, lambda_: int, m: int, *,
-                    root: int = 0, scratch=None, timing: Optional[Timing] = None):
+                    root: int = 0, scratch=None, timing: Optional[Timing] = None, flags: int = 0):
     """Host-buffer (pinned numpy / torch CPU) variant of `mw_product_device`:
     H2D of this rank's A rows (and B on root), the sharded product, C gathered
     on root and copied back into C_host.  `scratch` caches device buffers."""
@@ -115,7 +115,8 @@ def mw_product_host(A_rows_host, B_host, C_host, p: int, u: int, v: int, lambda_
         raise Error("non-root ranks must know n (pass scratch={'n': n})")
     dC = buf("Crows", (a.shape[0], n))
     dCf = buf("Cfull", (m, n)) if C_host is not None else None
-    mw_product_device(dA, dB, dC, p, u, v, lambda_, m, root=root, C_full=dCf, timing=timing)
+    mw_product_device(dA, dB, dC, p, u, v, lambda_, m, root=root, C_full=dCf, timing=timing,
+                      flags=flags)
     if C_host is not None:
         torch.as_tensor(C_host).copy_(dCf)
     torch.cuda.synchronize()

@@ -13,6 +13,16 @@ import paper_2601_07508_b200 as F
 
 pytestmark = pytest.mark.gpu
 
+
+@pytest.fixture(autouse=True, params=["dmma", "i8"])
+def engine(request):
+    """Every test runs on both engines: the FP64 DMMA multiword engine and the
+    int8 tcgen05 multiword engine (the library default)."""
+    F.set_default_engine(request.param)
+    yield request.param
+    F.set_default_engine(None)
+
+
 COMBOS = [(1, 1), (1, 2), (2, 1), (1, 3), (3, 1), (1, 4), (4, 1), (2, 2), (2, 3), (3, 2), (2, 4),
           (4, 2)]
 
@@ -44,14 +54,17 @@ def test_golden_vectors(golden):
     assert n_checked == len(golden["cases"])
 
 
-def test_config1_checksum():
+def test_config1_checksum(engine):
     """BASELINE config 1: 1024^3, 50-bit prime, (2,2), lambda 7 (reference C)."""
     p, A, B = O.seeded_inputs(1024, 1024, 1024, 50)
     tm = F.Timing()
     C = F.mw_product(A, B, 2, 2, 7, F.FpContext.make(p), timing=tm)
     assert C[0, 0] == 247707968029641 and C[-1, -1] == 526583644345359  # SURVEY Appendix B
     assert (C == O.exact_mod_gemm(A, B, p)).all()
-    assert tm.lambda_k == 28 and tm.launches == 3
+    assert tm.launches == 3
+    # exact K-block between reductions: 28 terms (DMMA, signed words) or an
+    # int32 segment of 147 x 64 terms (int8, 7 digits)
+    assert tm.lambda_k == (28 if engine == "dmma" else 9408)
 
 
 @pytest.mark.parametrize("u,v", COMBOS)
