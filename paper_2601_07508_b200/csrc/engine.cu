@@ -189,11 +189,11 @@ Job make_i8_job(i64 m, i64 k, i64 n, u64 p) {
   j.m = m, j.k = k, j.n = n, j.p = p, j.engine = kI8;
   j.D = std::max(1, (bitsize(p - 1) + 7) / 8);
   j.BM = i8::kBM;
-  j.BN = i8::kBN;
   j.MB = static_cast<int>((m + i8::kBM - 1) / i8::kBM);
-  j.NB = static_cast<int>((n + i8::kBN - 1) / i8::kBN);
   j.KB = static_cast<int>((k + i8::kBK - 1) / i8::kBK);
   dispatch_d(j.D, [&]<int D>() {
+    j.BN = i8::Cfg<D>::kNT;
+    j.NB = static_cast<int>((n + j.BN - 1) / j.BN);
     j.per_rb_bytes = static_cast<size_t>(j.KB) * i8::Cfg<D>::kAStage;
     j.apack_bytes = static_cast<size_t>(j.MB) * j.per_rb_bytes;
     j.bpack_bytes = static_cast<size_t>(j.NB) * j.KB * i8::Cfg<D>::kBStage;

@@ -30,24 +30,29 @@ namespace i8 {
 using i64 = std::int64_t;
 
 constexpr int kBM = 128;      // rows per CTA tile (MMA M)
-constexpr int kBN = 32;       // output columns per CTA tile
 constexpr int kBK = 64;       // k bytes (int8 elements) per pipeline stage
 constexpr int kKSteps = kBK / 32;  // MMA K = 32 for kind::i8
 constexpr int kThreads = 192;      // 6 warps
 
+// Output columns per CTA tile (NT): the widest multiple of 32 with
+// (2D-1) NT <= 512 TMEM columns and N_mma = D NT <= 256.  Wider tiles read
+// less shared memory per MMA (A is re-read once per MMA) and amortise the
+// per-tile epilogue over more work.
 template <int D>
 struct Cfg {
+  static constexpr int kNT = D == 1 ? 256 : D == 2 ? 128 : D <= 4 ? 64 : 32;
   static constexpr int kAStage = D * kBM * kBK;        // bytes: D digit tiles of 128 x 64
-  static constexpr int kBStage = D * kBN * kBK;        // bytes: B_cat tile of (32 D) x 64
+  static constexpr int kBStage = D * kNT * kBK;        // bytes: B_cat tile of (NT D) x 64
   static constexpr int kStageBytes = kAStage + kBStage;
   static constexpr int kStages = (220 * 1024) / kStageBytes > 8 ? 8 : (220 * 1024) / kStageBytes;
   static constexpr int kBlocks = 2 * D - 1;            // weight blocks s = 0 .. 2D-2
-  static constexpr int kTmemCols = kBlocks * kBN;
+  static constexpr int kTmemCols = kBlocks * kNT;
   static constexpr int kTmemAlloc = kTmemCols <= 32 ? 32 : kTmemCols <= 64 ? 64 : kTmemCols <= 128 ? 128
                                     : kTmemCols <= 256 ? 256 : 512;
   static constexpr int kSmem = kStages * kStageBytes + 1024;  // + barriers / tmem slot
-  static constexpr int kNmma = D * kBN;
+  static constexpr int kNmma = D * kNT;
   static_assert(kStages >= 2, "pipeline needs two stages");
+  static_assert(kTmemCols <= 512 && kNmma <= 256 && kNmma % 16 == 0, "tile does not fit the MMA / TMEM");
 };
 
 // ------------------------------------------------------------ descriptors
@@ -181,34 +186,36 @@ __global__ void __launch_bounds__(256) pack_a_i8(const double* __restrict__ A, i
   }
 }
 
-// B: k x n residues -> B_cat digit rows (digit j, column c) -> row 32 j + c,
+// B: k x n residues -> B_cat digit rows (digit j, column c) -> row NT j + c,
 // K-major.  Chunk (cb, kb) (contiguous, kBStage bytes):
-//   [k16 c (4)][row group g (4 D)][row r (8)][16 bytes]
-// A block transposes a 64 (k) x 32 (col) tile through shared memory.
+//   [k16 c (4)][row group g (NT D / 8)][row r (8)][16 bytes]
+// A block transposes 64 (k) x 32 (col) sub-tiles through shared memory.
 template <int D>
 __global__ void __launch_bounds__(256) pack_b_i8(const double* __restrict__ B, i64 ldb, i64 k, i64 n,
                                                  int KB, int NB, uint8_t* __restrict__ out) {
-  __shared__ unsigned long long tile[kBK][kBN + 1];
-  const i64 tiles = static_cast<i64>(KB) * NB;
+  constexpr int NT = Cfg<D>::kNT, SUB = NT / 32;
+  __shared__ unsigned long long tile[kBK][33];
+  const i64 tiles = static_cast<i64>(KB) * NB * SUB;
   for (i64 t = blockIdx.x; t < tiles; t += gridDim.x) {
-    const i64 cb = t % NB, kb = t / NB;
+    const int sb = static_cast<int>(t % SUB);
+    const i64 cb = (t / SUB) % NB, kb = t / (SUB * static_cast<i64>(NB));
     __syncthreads();
-    for (int e = threadIdx.x; e < kBK * kBN; e += blockDim.x) {
-      const int kr = e / kBN, cc = e % kBN;
-      const i64 kk = kb * kBK + kr, col = cb * kBN + cc;
+    for (int e = threadIdx.x; e < kBK * 32; e += blockDim.x) {
+      const int kr = e / 32, cc = e % 32;
+      const i64 kk = kb * kBK + kr, col = cb * NT + sb * 32 + cc;
       tile[kr][cc] = (kk < k && col < n) ? static_cast<unsigned long long>(B[kk * ldb + col]) : 0ull;
     }
     __syncthreads();
     uint8_t* base = out + (cb * KB + kb) * static_cast<i64>(Cfg<D>::kBStage);
-    // units: (digit j, column c, k16 chunk q): 16 bytes each
-    for (int u = threadIdx.x; u < D * kBN * (kBK / 16); u += blockDim.x) {
-      const int q = u % (kBK / 16), cc = (u / (kBK / 16)) % kBN, j = u / ((kBK / 16) * kBN);
+    // units: (digit j, column cc, k16 chunk q): 16 bytes each
+    for (int u = threadIdx.x; u < D * 32 * (kBK / 16); u += blockDim.x) {
+      const int q = u % (kBK / 16), cc = (u / (kBK / 16)) % 32, j = u / ((kBK / 16) * 32);
       uint32_t w[4] = {0, 0, 0, 0};
 #pragma unroll
       for (int e = 0; e < 16; ++e)
         w[e / 4] |= static_cast<uint32_t>((tile[q * 16 + e][cc] >> (8 * j)) & 0xFF) << (8 * (e % 4));
-      const int nn = j * kBN + cc, g = nn / 8, r8 = nn % 8;
-      *reinterpret_cast<uint4*>(base + ((q * (D * kBN / 8) + g) * 8 + r8) * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+      const int nn = j * NT + sb * 32 + cc, g = nn / 8, r8 = nn % 8;
+      *reinterpret_cast<uint4*>(base + ((q * (D * NT / 8) + g) * 8 + r8) * 16) = make_uint4(w[0], w[1], w[2], w[3]);
     }
   }
 }
@@ -292,7 +299,7 @@ __global__ void __launch_bounds__(kThreads, 1) mwi8_kernel(const __grid_constant
 #pragma unroll
             for (int i = 0; i < D; ++i) {
               const uint64_t ad = smem_desc(a0 + i * (kBM * kBK) + t * 2 * (kBM / 8) * 128, (kBM / 8) * 128, 128);
-              mma_i8(tbase + i * kBN, ad, bd, idesc, 1u);
+              mma_i8(tbase + i * CF::kNT, ad, bd, idesc, 1u);
             }
           }
           mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
@@ -306,12 +313,15 @@ __global__ void __launch_bounds__(kThreads, 1) mwi8_kernel(const __grid_constant
     const int row_in_tile = quad * 32 + lane;  // TMEM lane == tile row
     const uint32_t trow = tbase + (static_cast<uint32_t>(quad * 32) << 16);
     const unsigned long long p = P.p, mu = P.mu;
-    unsigned long long res[kBN];
-#pragma unroll
-    for (int c = 0; c < kBN; ++c) res[c] = 0;
+    constexpr int NT = CF::kNT;
+    const i64 row = static_cast<i64>(tm) * kBM + row_in_tile;
+    const i64 col_base = static_cast<i64>(tn) * NT;
+    double* dst_row = P.C + row * P.ldc + col_base;
     // zero the accumulators for the first segment
+#pragma unroll 1
+    for (int b = 0; b < CF::kBlocks; ++b)
 #pragma unroll
-    for (int b = 0; b < CF::kBlocks; ++b) tmem_st32_zero(trow + b * kBN);
+      for (int c0 = 0; c0 < NT; c0 += 32) tmem_st32_zero(trow + b * NT + c0);
     tmem_wait_st();
     fence_before();
     __syncwarp();
@@ -319,43 +329,49 @@ __global__ void __launch_bounds__(kThreads, 1) mwi8_kernel(const __grid_constant
     for (int seg = 0; seg < nseg; ++seg) {
       dev::mbar_wait(tmem_full, seg & 1);
       fence_after();
-      unsigned long long h[kBN];
-      uint32_t v[32];
-      tmem_ld32(trow + (CF::kBlocks - 1) * kBN, v);
-      tmem_wait_ld();
-#pragma unroll
-      for (int c = 0; c < kBN; ++c) h[c] = v[c] % p;
+      // 32 output columns at a time: Horner over the weight blocks, top down
 #pragma unroll 1
-      for (int b = CF::kBlocks - 2; b >= 0; --b) {
-        tmem_ld32(trow + b * kBN, v);
+      for (int c0 = 0; c0 < NT; c0 += 32) {
+        unsigned long long h[32];
+        uint32_t v[32];
+        tmem_ld32(trow + (CF::kBlocks - 1) * NT + c0, v);
         tmem_wait_ld();
 #pragma unroll
-        for (int c = 0; c < kBN; ++c) h[c] = barrett((h[c] << 8) + v[c], p, mu);
-      }
+        for (int c = 0; c < 32; ++c) h[c] = v[c] % p;
+#pragma unroll 1
+        for (int b = CF::kBlocks - 2; b >= 0; --b) {
+          tmem_ld32(trow + b * NT + c0, v);
+          tmem_wait_ld();
 #pragma unroll
-      for (int c = 0; c < kBN; ++c) {
-        const unsigned long long t = res[c] + h[c];
-        res[c] = t >= p ? t - p : t;
+          for (int c = 0; c < 32; ++c) h[c] = barrett((h[c] << 8) + v[c], p, mu);
+        }
+        if (row < P.m) {
+          double* dst = dst_row + c0;
+          const i64 col0 = col_base + c0;
+          if (seg > 0) {  // earlier segments' residues were parked in C by this thread
+            for (int c = 0; c < 32 && col0 + c < P.n; ++c) {
+              const unsigned long long t = h[c] + static_cast<unsigned long long>(dst[c]);
+              h[c] = t >= p ? t - p : t;
+            }
+          }
+          if (col0 + 32 <= P.n && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+#pragma unroll
+            for (int c = 0; c < 32; c += 2)
+              *reinterpret_cast<double2*>(dst + c) = make_double2(static_cast<double>(h[c]), static_cast<double>(h[c + 1]));
+          } else {
+            for (int c = 0; c < 32 && col0 + c < P.n; ++c) dst[c] = static_cast<double>(h[c]);
+          }
+        }
       }
       if (seg + 1 < nseg) {  // re-zero and hand the accumulators back to the MMA warp
+#pragma unroll 1
+        for (int b = 0; b < CF::kBlocks; ++b)
 #pragma unroll
-        for (int b = 0; b < CF::kBlocks; ++b) tmem_st32_zero(trow + b * kBN);
+          for (int c0 = 0; c0 < NT; c0 += 32) tmem_st32_zero(trow + b * NT + c0);
         tmem_wait_st();
         fence_before();
         __syncwarp();
         if (lane == 0) dev::mbar_arrive(tmem_empty);
-      }
-    }
-    const i64 row = static_cast<i64>(tm) * kBM + row_in_tile;
-    const i64 col0 = static_cast<i64>(tn) * kBN;
-    if (row < P.m) {
-      double* dst = P.C + row * P.ldc + col0;
-      if (col0 + kBN <= P.n && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-#pragma unroll
-        for (int c = 0; c < kBN; c += 2)
-          *reinterpret_cast<double2*>(dst + c) = make_double2(static_cast<double>(res[c]), static_cast<double>(res[c + 1]));
-      } else {
-        for (int c = 0; c < kBN && col0 + c < P.n; ++c) dst[c] = static_cast<double>(res[c]);
       }
     }
   }
