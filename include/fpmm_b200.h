@@ -175,6 +175,20 @@ int fpmm_b200_accumulate_device(double* dC, int64_t ldc, const double* dA, int64
                                 const double* dB, int64_t ldb, int64_t m, int64_t w, int64_t n,
                                 int device, void* stream);
 
+/* ------------------------------------------ prepared (resident) A words */
+/* The unbalanced scenario (driver.cpp:215-218) reuses A's
+ * word decomposition across iterated products: decompose / pack A once,
+ * keep the words resident in HBM, multiply by many B.  The engine flag of
+ * prepare_a fixes the engine of every product made from the handle. */
+typedef struct fpmm_b200_prepared fpmm_b200_prepared;
+int fpmm_b200_prepare_a_device(const double* dA, int64_t lda, int64_t m, int64_t k, uint64_t p, int u, int v,
+                               unsigned flags, int device, void* stream, fpmm_b200_prepared** out);
+/* C (m x n) = A B mod p from the prepared A (mw_product_words with fixed da) */
+int fpmm_b200_mw_product_prepared_device(const fpmm_b200_prepared* a, const double* dB, int64_t ldb, double* dC,
+                                         int64_t ldc, int64_t n, uint64_t lambda, void* stream, unsigned flags,
+                                         fpmm_b200_timing* timing);
+int fpmm_b200_prepared_free(fpmm_b200_prepared* a);
+
 /* ------------------------------------- multi-process partitioner (NCCL) */
 /* One process per GPU.  Rank 0 creates the id, the host bootstrap (e.g. a
  * torch.distributed / MPI broadcast) ships the 128 bytes to every rank. */

@@ -203,6 +203,25 @@ int fpmm_b200_accumulate_device(double* dC, int64_t ldc, const double* dA, int64
   return guarded([&] { accumulate_device(dC, ldc, dA, lda, dB, ldb, m, w, n, device, stream); });
 }
 
+int fpmm_b200_prepare_a_device(const double* dA, int64_t lda, int64_t m, int64_t k, uint64_t p, int u, int v,
+                               unsigned flags, int device, void* stream, fpmm_b200_prepared** out) {
+  return guarded([&] {
+    *out = reinterpret_cast<fpmm_b200_prepared*>(prepare_a_device(dA, lda, m, k, p, u, v, flags, device, stream));
+  });
+}
+
+int fpmm_b200_mw_product_prepared_device(const fpmm_b200_prepared* a, const double* dB, int64_t ldb, double* dC,
+                                         int64_t ldc, int64_t n, uint64_t lambda, void* stream, unsigned flags,
+                                         fpmm_b200_timing* timing) {
+  return guarded([&] {
+    product_prepared_device(reinterpret_cast<const Prepared*>(a), dB, ldb, dC, ldc, n, lambda, stream, flags, timing);
+  });
+}
+
+int fpmm_b200_prepared_free(fpmm_b200_prepared* a) {
+  return guarded([&] { prepared_free(reinterpret_cast<Prepared*>(a)); });
+}
+
 int fpmm_b200_nccl_id_size(void) { return nccl_id_size(); }
 int fpmm_b200_nccl_get_unique_id(void* id) {
   return guarded([&] { nccl_unique_id(id); });

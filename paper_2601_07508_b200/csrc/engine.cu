@@ -63,7 +63,7 @@ struct DeviceCtx {
   int dev = -1;
   cudaStream_t stream = nullptr, s_in = nullptr, s_out = nullptr;
   cudaEvent_t ev[8] = {}, ev_in[kChunks] = {}, ev_out[kChunks] = {};
-  DevBuf apack, bpack, a, b, c, tmp, err;
+  DevBuf apack, bpack, a, b, c, tmp, err, splitws;
   void init(int d) {
     dev = d;
     CUDA_OK(cudaSetDevice(d));
@@ -87,6 +87,7 @@ struct DeviceCtx {
     if (s_out) cudaStreamDestroy(s_out), s_out = nullptr;
     if (stream) cudaStreamDestroy(stream), stream = nullptr;
     apack.release(), bpack.release(), a.release(), b.release(), c.release(), tmp.release(), err.release();
+    splitws.release();
     dev = -1;
   }
 };
@@ -205,6 +206,8 @@ Job make_i8_job(i64 m, i64 k, i64 n, u64 p) {
   i8::Params& q = j.ip;
   q.m = m, q.n = n, q.MB = j.MB, q.NB = j.NB, q.KB = j.KB;
   q.seg_kb = static_cast<int>(std::min<i64>(seg_kb, j.KB > 0 ? j.KB : 1));
+  q.kb_per_split = j.KB;
+  q.split_stride = 0;
   q.p = p;
   q.mu = static_cast<unsigned long long>((static_cast<u128>(1) << 64) / p);
   return j;
@@ -309,6 +312,26 @@ void launch_gemm_i8(const Job& j, const void* apack, const void* bpack, double* 
   q.ldc = ldc;
   q.m = rows;
   q.MB = static_cast<int>((rows + i8::kBM - 1) / i8::kBM);
+  // split-K when the output has too few tiles to fill two waves of 148 SMs
+  // (tall-and-skinny / unbalanced shapes): slices of >= 16 k-blocks write
+  // partial residues to a workspace, combined mod p afterwards
+  const i64 tiles0 = static_cast<i64>(q.MB) * q.NB;
+  int splits = 1;
+  if (tiles0 > 0 && tiles0 < 2 * 148) {
+    const i64 want = (2 * 148 + tiles0 - 1) / tiles0;
+    splits = static_cast<int>(std::max<i64>(1, std::min<i64>({want, j.KB / 16, 32})));
+  }
+  q.kb_per_split = (j.KB + splits - 1) / splits;
+  splits = (j.KB + q.kb_per_split - 1) / q.kb_per_split;
+  double* work = nullptr;
+  if (splits > 1) {
+    int dev = 0;
+    CUDA_OK(cudaGetDevice(&dev));
+    work = static_cast<double*>(ctx(dev).splitws.get(sizeof(double) * splits * rows * j.n));
+    q.C = work;
+    q.ldc = j.n;
+    q.split_stride = rows * j.n;
+  }
   dispatch_d(j.D, [&]<int D>() {
     using CF = i8::Cfg<D>;
     auto kern = i8::mwi8_kernel<D>;
@@ -321,9 +344,14 @@ void launch_gemm_i8(const Job& j, const void* apack, const void* bpack, double* 
     }
     const i64 tiles = static_cast<i64>(q.MB) * q.NB;
     if (tiles > 0x7fffffff) throw Failure(FPMM_B200_EERROR, "problem too large for one launch");
-    kern<<<static_cast<unsigned>(tiles), i8::kThreads, CF::kSmem, s>>>(q);
+    kern<<<dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(splits)), i8::kThreads, CF::kSmem, s>>>(q);
   });
   CUDA_OK(cudaGetLastError());
+  if (splits > 1) {
+    i8::splitk_reduce_kernel<<<grid_for(rows * j.n, 256), 256, 0, s>>>(work, rows * j.n, splits, C, ldc, rows,
+                                                                        j.n, j.p);
+    CUDA_OK(cudaGetLastError());
+  }
 }
 
 void launch_gemm(const Job& j, const void* apack_v, const void* bpack_v, double* C, i64 ldc, i64 rows,
@@ -435,6 +463,95 @@ void product_device(const ProductArgs& a, int device, void* stream, fpmm_b200_ti
     tm->ngpus = 1;
   }
   if (!(a.flags & FPMM_B200_ASYNC)) CUDA_OK(cudaStreamSynchronize(s));
+}
+
+// ------------------------------------------------- prepared (resident) A words
+// The unbalanced scenario of the paper (and run_bench's, driver.cpp:215-218)
+// reuses A's decomposition across many products: pack A's words once, keep
+// them resident in HBM, and run each product from the packed words.
+struct Prepared {
+  int device = 0, engine = kI8;
+  u64 p = 0;
+  int u = 1, v = 1;
+  i64 m = 0, k = 0;
+  unsigned flags = 0;
+  DevBuf words;
+};
+
+Prepared* prepare_a_device(const double* dA, i64 lda, i64 m, i64 k, u64 p, int u, int v, unsigned flags,
+                           int device, void* stream) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (m < 0 || k < 0) throw Failure(FPMM_B200_EERROR, "matrix dimensions must be nonnegative");
+  context_check(p, (flags & FPMM_B200_ALLOW_COMPOSITE) != 0);
+  if (u < 1 || v < 1) throw Failure(FPMM_B200_EERROR, "multiword product: word counts must be positive");
+  DeviceCtx& c = ctx(device);
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c.stream;
+  auto h = std::make_unique<Prepared>();
+  h->device = device, h->engine = resolve_engine(flags), h->p = p, h->u = u, h->v = v, h->m = m, h->k = k;
+  h->flags = flags;
+  if (m > 0 && k > 0) {
+    const Job j = make_job(m, k, 1, p, u, v, h->engine);
+    void* w = h->words.get(j.apack_bytes);
+    int* err = nullptr;
+    if (flags & FPMM_B200_CHECK_INPUTS) {
+      err = static_cast<int*>(c.err.get(sizeof(int)));
+      CUDA_OK(cudaMemsetAsync(err, 0, sizeof(int), s));
+    }
+    launch_pack_a(j, dA, lda, m, w, err, s);
+    if (err) check_err_flag(c, s);
+    CUDA_OK(cudaStreamSynchronize(s));
+  }
+  return h.release();
+}
+
+void prepared_free(Prepared* h) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (!h) return;
+  cudaSetDevice(h->device);
+  h->words.release();
+  delete h;
+}
+
+void product_prepared_device(const Prepared* h, const double* dB, i64 ldb, double* dC, i64 ldc, i64 n, u64 lambda,
+                             void* stream, unsigned flags, fpmm_b200_timing* tm) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (!h) throw Failure(FPMM_B200_EERROR, "null prepared operand");
+  const unsigned fl = (flags & ~(FPMM_B200_ENGINE_DMMA | FPMM_B200_ENGINE_I8)) |
+                      (h->engine == kI8 ? FPMM_B200_ENGINE_I8 : FPMM_B200_ENGINE_DMMA) |
+                      (h->flags & FPMM_B200_ALLOW_COMPOSITE);
+  validate_product(h->p, h->u, h->v, lambda, h->m, h->k, n, fl);
+  DeviceCtx& c = ctx(h->device);
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c.stream;
+  if (tm) *tm = fpmm_b200_timing{};
+  if (h->m == 0 || n == 0) return;
+  if (h->k == 0) {
+    zero_c(dC, ldc, h->m, n, s);
+    if (!(fl & FPMM_B200_ASYNC)) CUDA_OK(cudaStreamSynchronize(s));
+    return;
+  }
+  const Job j = make_job(h->m, h->k, n, h->p, h->u, h->v, h->engine);
+  void* bpack = c.bpack.get(j.bpack_bytes);
+  int* err = nullptr;
+  if (fl & FPMM_B200_CHECK_INPUTS) {
+    err = static_cast<int*>(c.err.get(sizeof(int)));
+    CUDA_OK(cudaMemsetAsync(err, 0, sizeof(int), s));
+  }
+  if (tm) CUDA_OK(cudaEventRecord(c.ev[0], s));
+  launch_pack_b(j, dB, ldb, bpack, err, s);
+  if (tm) CUDA_OK(cudaEventRecord(c.ev[1], s));
+  launch_gemm(j, h->words.ptr, bpack, dC, ldc, h->m, s);
+  if (tm) CUDA_OK(cudaEventRecord(c.ev[2], s));
+  if (err) check_err_flag(c, s);
+  if (tm) {
+    CUDA_OK(cudaEventSynchronize(c.ev[2]));
+    tm->pack_ms = elapsed(c.ev[0], c.ev[1]);
+    tm->gemm_ms = elapsed(c.ev[1], c.ev[2]);
+    tm->total_ms = elapsed(c.ev[0], c.ev[2]);
+    tm->lambda_k = j.lambda_k;
+    tm->launches = 2;
+    tm->ngpus = 1;
+  }
+  if (!(fl & FPMM_B200_ASYNC)) CUDA_OK(cudaStreamSynchronize(s));
 }
 
 // ------------------------------------------------------------- host buffers

@@ -35,6 +35,13 @@ void product_words_host(const double* Aw, i64 a_stride, i64 lda, u64 alpha, int 
                         i64 b_stride, i64 ldb, u64 beta, int v, double* C, i64 ldc, i64 m, i64 k,
                         i64 n, u64 p, u64 lambda, unsigned flags, fpmm_b200_timing* tm);
 
+struct Prepared;
+Prepared* prepare_a_device(const double* dA, i64 lda, i64 m, i64 k, u64 p, int u, int v, unsigned flags,
+                           int device, void* stream);
+void prepared_free(Prepared* h);
+void product_prepared_device(const Prepared* h, const double* dB, i64 ldb, double* dC, i64 ldc, i64 n, u64 lambda,
+                             void* stream, unsigned flags, fpmm_b200_timing* tm);
+
 void decompose_device(const double* dM, i64 ld, i64 rows, i64 cols, u64 p, int u, double* dwords,
                       i64 word_stride, u64* base, int device, void* stream);
 void decompose_host(const double* M, i64 ld, i64 rows, i64 cols, u64 p, int u, double* words,

@@ -139,6 +139,8 @@ struct Params {
   i64 ldc, m, n;
   int MB, NB, KB;       // tiles along m, n and 64-byte k-blocks
   int seg_kb;           // k-blocks per exact accumulation segment
+  int kb_per_split;     // split-K: k-blocks per blockIdx.y slice (== KB when unsplit)
+  i64 split_stride;     // split-K: C offset (elements) between the slices' partial outputs
   unsigned long long p, mu;
 };
 
@@ -244,7 +246,10 @@ __global__ void __launch_bounds__(kThreads, 1) mwi8_kernel(const __grid_constant
   const int gsz = min(P.MB - first_m, GROUP);
   const int tm = first_m + (static_cast<int>(blockIdx.x) % in_group) % gsz;
   const int tn = (static_cast<int>(blockIdx.x) % in_group) / gsz;
-  const int nseg = (P.KB + P.seg_kb - 1) / P.seg_kb;
+  // split-K slice of this CTA (blockIdx.y): k-blocks [kb0, kb0 + nkb)
+  const int kb0 = static_cast<int>(blockIdx.y) * P.kb_per_split;
+  const int nkb = max(0, min(P.KB, kb0 + P.kb_per_split) - kb0);
+  const int nseg = max(1, (nkb + P.seg_kb - 1) / P.seg_kb);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -269,9 +274,9 @@ __global__ void __launch_bounds__(kThreads, 1) mwi8_kernel(const __grid_constant
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
-      const uint8_t* gA = P.apack + static_cast<i64>(tm) * P.KB * CF::kAStage;
-      const uint8_t* gB = P.bpack + static_cast<i64>(tn) * P.KB * CF::kBStage;
-      for (int kb = 0; kb < P.KB; ++kb) {
+      const uint8_t* gA = P.apack + (static_cast<i64>(tm) * P.KB + kb0) * CF::kAStage;
+      const uint8_t* gB = P.bpack + (static_cast<i64>(tn) * P.KB + kb0) * CF::kBStage;
+      for (int kb = 0; kb < nkb; ++kb) {
         const int s = kb % S;
         if (kb >= S) dev::mbar_wait(&empty[s], ((kb / S) - 1) & 1);
         dev::mbar_arrive_expect_tx(&full[s], CF::kStageBytes);
@@ -283,11 +288,11 @@ __global__ void __launch_bounds__(kThreads, 1) mwi8_kernel(const __grid_constant
     // ---------------- MMA issuer (one thread) ----------------
     if (lane == 0) {
       constexpr uint32_t idesc = instr_desc(kBM, CF::kNmma);
-      int kb = 0;
+      int kb = 0;  // relative to kb0
       for (int seg = 0; seg < nseg; ++seg) {
         dev::mbar_wait(tmem_empty, seg & 1);  // epilogue zeroed / drained the accumulators
         fence_after();
-        const int kend = min(P.KB, kb + P.seg_kb);
+        const int kend = min(nkb, kb + P.seg_kb);
         for (; kb < kend; ++kb) {
           const int s = kb % S;
           dev::mbar_wait(&full[s], (kb / S) & 1);
@@ -316,7 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1) mwi8_kernel(const __grid_constant
     constexpr int NT = CF::kNT;
     const i64 row = static_cast<i64>(tm) * kBM + row_in_tile;
     const i64 col_base = static_cast<i64>(tn) * NT;
-    double* dst_row = P.C + row * P.ldc + col_base;
+    double* dst_row = P.C + static_cast<i64>(blockIdx.y) * P.split_stride + row * P.ldc + col_base;
     // zero the accumulators for the first segment
 #pragma unroll 1
     for (int b = 0; b < CF::kBlocks; ++b)
@@ -380,6 +385,20 @@ __global__ void __launch_bounds__(kThreads, 1) mwi8_kernel(const __grid_constant
   if (warp == 1) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tbase), "r"(CF::kTmemAlloc));
+  }
+}
+
+// split-K combine: C[i][j] = sum_s W[s][i][j] mod p (W slices are residues)
+__global__ void splitk_reduce_kernel(const double* __restrict__ W, i64 slice, int splits, double* __restrict__ C,
+                                     i64 ldc, i64 rows, i64 cols, unsigned long long p) {
+  for (i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; e < rows * cols;
+       e += static_cast<i64>(gridDim.x) * blockDim.x) {
+    unsigned long long acc = 0;
+    for (int s = 0; s < splits; ++s) {
+      acc += static_cast<unsigned long long>(W[s * slice + e]);
+      acc -= acc >= p ? p : 0;
+    }
+    C[(e / cols) * ldc + e % cols] = static_cast<double>(acc);
   }
 }
 

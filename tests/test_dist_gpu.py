@@ -1,0 +1,65 @@
+"""The one-process-per-GPU partitioner on a real GPU (world_size 1: only one
+B200 is available to the tests).  Exercises the run-time NCCL binding,
+communicator set-up, the B-word broadcast and the C gather on root."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2601_07508_b200 as F
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+@pytest.mark.parametrize("engine", ["i8", "dmma"])
+def test_dist_world1_gather(engine):
+    import torch
+    import torch.distributed as td
+    from paper_2601_07508_b200 import dist as D
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()))
+    td.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        part = D.init_from_torch(0)
+        m, k, n, bits = 300, 200, 70, 52
+        p, A, B = O.seeded_inputs(m, k, n, bits)
+        pl = F.plan_for_modulus(p, m, k, n)
+        r0, rn = part.rows_for(m, pl.u, pl.v)
+        assert (r0, rn) == (0, m)
+        dA = torch.from_numpy(A).cuda()
+        dB = torch.from_numpy(B).cuda()
+        dCr = torch.empty((rn, n), dtype=torch.float64, device="cuda")
+        dCf = torch.empty((m, n), dtype=torch.float64, device="cuda")
+        eng = F.ENGINE_I8 if engine == "i8" else F.ENGINE_DMMA
+        tm = F.Timing()
+        D.mw_product_device(dA, dB, dCr, p, pl.u, pl.v, pl.lambda_, m, root=0, C_full=dCf, flags=eng,
+                            timing=tm)
+        want = O.exact_mod_gemm(A, B, p)
+        assert (dCr.cpu().numpy() == want).all()
+        assert (dCf.cpu().numpy() == want).all()
+        # host-buffer variant (the bench's e2e path at N > 1)
+        hC = torch.empty((m, n), dtype=torch.float64).pin_memory()
+        D.mw_product_host(torch.from_numpy(A).pin_memory(), torch.from_numpy(B).pin_memory(), hC, p,
+                          pl.u, pl.v, pl.lambda_, m, root=0, flags=eng)
+        assert (hC.numpy() == want).all()
+        D.finalize()
+    finally:
+        td.destroy_process_group()
+
+
+def test_in_process_ngpus1_equals_default():
+    p, A, B = O.seeded_inputs(257, 130, 99, 47)
+    pl = F.plan_for_modulus(p, 257, 130, 99)
+    C = F.mw_product(A, B, pl.u, pl.v, pl.lambda_, F.FpContext.make(p), ngpus=1)
+    assert (C == O.exact_mod_gemm(A, B, p)).all()
+    with pytest.raises(F.Error):
+        F.mw_product(A, B, pl.u, pl.v, pl.lambda_, F.FpContext.make(p), ngpus=F.device_count() + 1)

@@ -251,3 +251,39 @@ def test_multi_gpu_in_process():
     C1 = F.mw_product(A, B, 2, 2, 7, F.FpContext.make(p))
     for g in range(2, n + 1):
         assert (F.mw_product(A, B, 2, 2, 7, F.FpContext.make(p), ngpus=g) == C1).all()
+
+
+def test_prepared_a_unbalanced_split_k():
+    """Unbalanced scenario (m x k x 32, A's words resident and reused across
+    products, driver.cpp:215-218); few output tiles force split-K."""
+    import torch
+    m, k, n = 1093, 3277, 32
+    for bits in (20, 35, 50):
+        p, A, _ = O.seeded_inputs(m, k, n, bits)
+        pl = F.plan_for_modulus(p, m, k, n)
+        pa = F.PreparedA(torch.from_numpy(A).cuda(), p, pl.u, pl.v)
+        rng = np.random.default_rng(bits)
+        for _ in range(2):
+            B = rng.integers(0, p, size=(k, n)).astype(np.float64)
+            dC = torch.empty((m, n), dtype=torch.float64, device="cuda")
+            pa.product(torch.from_numpy(B).cuda(), dC, pl.lambda_)
+            assert (dC.cpu().numpy() == O.exact_mod_gemm(A, B, p)).all(), bits
+        pa.close()
+
+
+def test_unbalanced_preset_full_size():
+    """The paper's unbalanced preset 10923 x 32768 x 32 at 48 bits."""
+    import torch
+    m, k, n, bits = 10923, 32768, 32, 48
+    p = F.prev_prime(1 << bits)
+    dA = torch.empty((m, k), dtype=torch.float64, device="cuda")
+    dB = torch.empty((k, n), dtype=torch.float64, device="cuda")
+    F.random_residues_device(dA, p, 11)
+    F.random_residues_device(dB, p, 12)
+    pl = F.plan_for_modulus(p, m, k, n)
+    pa = F.PreparedA(dA, p, pl.u, pl.v)
+    dC = torch.empty((m, n), dtype=torch.float64, device="cuda")
+    pa.product(dB, dC, pl.lambda_)
+    A, B, Cm = dA.cpu().numpy(), dB.cpu().numpy(), dC.cpu().numpy()
+    assert O.freivalds(A, B, Cm, p, trials=2) == 0
+    pa.close()
