@@ -63,7 +63,7 @@ struct DeviceCtx {
   int dev = -1;
   cudaStream_t stream = nullptr, s_in = nullptr, s_out = nullptr;
   cudaEvent_t ev[8] = {}, ev_in[kChunks] = {}, ev_out[kChunks] = {};
-  DevBuf apack, bpack, a, b, c, tmp, err, splitws;
+  DevBuf apack, bpack, a, b, c, tmp, err, splitws, scratch;
   void init(int d) {
     dev = d;
     CUDA_OK(cudaSetDevice(d));
@@ -88,6 +88,7 @@ struct DeviceCtx {
     if (stream) cudaStreamDestroy(stream), stream = nullptr;
     apack.release(), bpack.release(), a.release(), b.release(), c.release(), tmp.release(), err.release();
     splitws.release();
+    scratch.release();
     dev = -1;
   }
 };
@@ -207,7 +208,13 @@ Job make_i8_job(i64 m, i64 k, i64 n, u64 p) {
   q.m = m, q.n = n, q.MB = j.MB, q.NB = j.NB, q.KB = j.KB;
   q.seg_kb = static_cast<int>(std::min<i64>(seg_kb, j.KB > 0 ? j.KB : 1));
   q.kb_per_split = j.KB;
+  q.splits = 1;
   q.split_stride = 0;
+  // epilogue reconstruction constants: 256^s mod p and Shoup quotients
+  for (int s = 0; s < 2 * j.D - 1 && s < 13; ++s) {
+    q.gam[s] = powmod(256 % p, static_cast<u64>(s), p);
+    q.gam_sh[s] = shoup(q.gam[s], p);
+  }
   q.p = p;
   q.mu = static_cast<unsigned long long>((static_cast<u128>(1) << 64) / p);
   return j;
@@ -323,15 +330,24 @@ void launch_gemm_i8(const Job& j, const void* apack, const void* bpack, double* 
   }
   q.kb_per_split = (j.KB + splits - 1) / splits;
   splits = (j.KB + q.kb_per_split - 1) / q.kb_per_split;
+  q.splits = splits;
+  int dev = 0;
+  CUDA_OK(cudaGetDevice(&dev));
+  DeviceCtx& dc = ctx(dev);
   double* work = nullptr;
   if (splits > 1) {
-    int dev = 0;
-    CUDA_OK(cudaGetDevice(&dev));
-    work = static_cast<double*>(ctx(dev).splitws.get(sizeof(double) * splits * rows * j.n));
+    work = static_cast<double*>(dc.splitws.get(sizeof(double) * splits * rows * j.n));
     q.C = work;
     q.ldc = j.n;
     q.split_stride = rows * j.n;
   }
+  // persistent grid: one CTA per SM (at most one work item each if fewer)
+  int sms = 148;
+  CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const i64 items = static_cast<i64>(q.MB) * q.NB * splits;
+  const unsigned grid = static_cast<unsigned>(std::max<i64>(1, std::min<i64>(items, sms)));
+  q.scratch = static_cast<uint32_t*>(
+      dc.scratch.get(sizeof(uint32_t) * static_cast<size_t>(grid) * i8::kBM * (2 * j.D - 1) * j.BN));
   dispatch_d(j.D, [&]<int D>() {
     using CF = i8::Cfg<D>;
     auto kern = i8::mwi8_kernel<D>;
@@ -342,9 +358,8 @@ void launch_gemm_i8(const Job& j, const void* apack, const void* bpack, double* 
       CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::kSmem));
       configured[dev & 63] = true;
     }
-    const i64 tiles = static_cast<i64>(q.MB) * q.NB;
-    if (tiles > 0x7fffffff) throw Failure(FPMM_B200_EERROR, "problem too large for one launch");
-    kern<<<dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(splits)), i8::kThreads, CF::kSmem, s>>>(q);
+    if (items > 0x7fffffff) throw Failure(FPMM_B200_EERROR, "problem too large for one launch");
+    kern<<<grid, i8::kThreads, CF::kSmem, s>>>(q);
   });
   CUDA_OK(cudaGetLastError());
   if (splits > 1) {

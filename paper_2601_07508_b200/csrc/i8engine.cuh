@@ -139,9 +139,12 @@ struct Params {
   i64 ldc, m, n;
   int MB, NB, KB;       // tiles along m, n and 64-byte k-blocks
   int seg_kb;           // k-blocks per exact accumulation segment
-  int kb_per_split;     // split-K: k-blocks per blockIdx.y slice (== KB when unsplit)
+  int kb_per_split;     // split-K: k-blocks per slice (== KB when unsplit)
+  int splits;           // split-K: number of slices
   i64 split_stride;     // split-K: C offset (elements) between the slices' partial outputs
   unsigned long long p, mu;
+  unsigned long long gam[13], gam_sh[13];  // 256^s mod p and Shoup constants, s = 0 .. 2D-2
+  uint32_t* scratch;    // per-CTA TMEM drain area: gridDim.x x 128 x (2D-1) NT u32
 };
 
 // --------------------------------------------------------------- packing
@@ -223,10 +226,43 @@ __global__ void __launch_bounds__(256) pack_b_i8(const double* __restrict__ B, i
 }
 
 // ------------------------------------------------------------------ GEMM
+// Work item t (0 <= t < MB * NB * splits) -> output tile (tm, tn), split ks.
+// Grouped rasterisation: the 148 items in flight cover GROUP tile-rows x ~37
+// tile-columns, so their A panels (GROUP x 7 MB at D=7, K=8192) and B_cat
+// panels stay resident in the 126 MB L2.
+struct Item {
+  int tm, tn, ks;
+};
+__device__ __forceinline__ Item item_of(int t, const Params& P) {
+  constexpr int GROUP = 4;
+  const int tiles = P.MB * P.NB;
+  const int r = t % tiles;
+  const int in_group = GROUP * P.NB;
+  const int first_m = (r / in_group) * GROUP;
+  const int gsz = min(P.MB - first_m, GROUP);
+  Item it;
+  it.tm = first_m + (r % in_group) % gsz;
+  it.tn = (r % in_group) / gsz;
+  it.ks = t / tiles;
+  return it;
+}
+
+// x * g mod p for x < 2^32 (Shoup: gs = floor(g 2^64 / p)); result in [0, p)
+__device__ __forceinline__ uint64_t shoup32(uint32_t x, uint64_t g, uint64_t gs, uint64_t p) {
+  const uint64_t q = __umul64hi(static_cast<uint64_t>(x), gs);
+  const uint64_t r = static_cast<uint64_t>(x) * g - q * p;
+  return r >= p ? r - p : r;
+}
+
+// Persistent: one CTA per SM loops over work items.  TMEM holds one set of
+// 2D-1 weight blocks; the epilogue drains it to a per-CTA L2-resident scratch
+// (a few microseconds), re-zeroes it and releases it to the MMA warp, then
+// reconstructs C = sum_s 256^s T_s mod p from the scratch while the tensor
+// cores already run the next item.
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1) mwi8_kernel(const __grid_constant__ Params P) {
   using CF = Cfg<D>;
-  constexpr int S = CF::kStages;
+  constexpr int S = CF::kStages, NT = CF::kNT, NB_ = CF::kBlocks;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * CF::kAStage;
@@ -237,19 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1) mwi8_kernel(const __grid_constant
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  // grouped rasterisation: a wave of 148 CTAs covers GROUP tile-rows x ~37
-  // tile-columns, so its A panels (GROUP x 7 MB at D=7, K=8192) and B_cat
-  // panels (37 x 1.8 MB) stay resident in the 126 MB L2
-  constexpr int GROUP = 4;
-  const int in_group = GROUP * P.NB;
-  const int first_m = (static_cast<int>(blockIdx.x) / in_group) * GROUP;
-  const int gsz = min(P.MB - first_m, GROUP);
-  const int tm = first_m + (static_cast<int>(blockIdx.x) % in_group) % gsz;
-  const int tn = (static_cast<int>(blockIdx.x) % in_group) / gsz;
-  // split-K slice of this CTA (blockIdx.y): k-blocks [kb0, kb0 + nkb)
-  const int kb0 = static_cast<int>(blockIdx.y) * P.kb_per_split;
-  const int nkb = max(0, min(P.KB, kb0 + P.kb_per_split) - kb0);
-  const int nseg = max(1, (nkb + P.seg_kb - 1) / P.seg_kb);
+  const int total = P.MB * P.NB * P.splits;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -274,42 +298,55 @@ __global__ void __launch_bounds__(kThreads, 1) mwi8_kernel(const __grid_constant
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
-      const uint8_t* gA = P.apack + (static_cast<i64>(tm) * P.KB + kb0) * CF::kAStage;
-      const uint8_t* gB = P.bpack + (static_cast<i64>(tn) * P.KB + kb0) * CF::kBStage;
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % S;
-        if (kb >= S) dev::mbar_wait(&empty[s], ((kb / S) - 1) & 1);
-        dev::mbar_arrive_expect_tx(&full[s], CF::kStageBytes);
-        dev::bulk_g2s(sA + s * CF::kAStage, gA + static_cast<i64>(kb) * CF::kAStage, CF::kAStage, &full[s]);
-        dev::bulk_g2s(sB + s * CF::kBStage, gB + static_cast<i64>(kb) * CF::kBStage, CF::kBStage, &full[s]);
+      int g = 0;  // k-blocks issued by this CTA (stage ring position)
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const Item it = item_of(t, P);
+        const int kb0 = it.ks * P.kb_per_split;
+        const int nkb = max(0, min(P.KB, kb0 + P.kb_per_split) - kb0);
+        const uint8_t* gA = P.apack + (static_cast<i64>(it.tm) * P.KB + kb0) * CF::kAStage;
+        const uint8_t* gB = P.bpack + (static_cast<i64>(it.tn) * P.KB + kb0) * CF::kBStage;
+        for (int kb = 0; kb < nkb; ++kb, ++g) {
+          const int s = g % S;
+          if (g >= S) dev::mbar_wait(&empty[s], ((g / S) - 1) & 1);
+          dev::mbar_arrive_expect_tx(&full[s], CF::kStageBytes);
+          dev::bulk_g2s(sA + s * CF::kAStage, gA + static_cast<i64>(kb) * CF::kAStage, CF::kAStage, &full[s]);
+          dev::bulk_g2s(sB + s * CF::kBStage, gB + static_cast<i64>(kb) * CF::kBStage, CF::kBStage, &full[s]);
+        }
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (one thread) ----------------
     if (lane == 0) {
       constexpr uint32_t idesc = instr_desc(kBM, CF::kNmma);
-      int kb = 0;  // relative to kb0
-      for (int seg = 0; seg < nseg; ++seg) {
-        dev::mbar_wait(tmem_empty, seg & 1);  // epilogue zeroed / drained the accumulators
-        fence_after();
-        const int kend = min(nkb, kb + P.seg_kb);
-        for (; kb < kend; ++kb) {
-          const int s = kb % S;
-          dev::mbar_wait(&full[s], (kb / S) & 1);
+      int g = 0, e = 0;  // stage ring position, accumulator generation
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const Item it = item_of(t, P);
+        const int kb0 = it.ks * P.kb_per_split;
+        const int nkb = max(0, min(P.KB, kb0 + P.kb_per_split) - kb0);
+        const int nseg = max(1, (nkb + P.seg_kb - 1) / P.seg_kb);
+        int kb = 0;
+        for (int seg = 0; seg < nseg; ++seg, ++e) {
+          dev::mbar_wait(tmem_empty, e & 1);  // epilogue drained and re-zeroed the accumulators
           fence_after();
-          const uint32_t a0 = dev::smem_u32(sA + s * CF::kAStage), b0 = dev::smem_u32(sB + s * CF::kBStage);
+          const int kend = min(nkb, kb + P.seg_kb);
+          for (; kb < kend; ++kb, ++g) {
+            const int s = g % S;
+            dev::mbar_wait(&full[s], (g / S) & 1);
+            fence_after();
+            const uint32_t a0 = dev::smem_u32(sA + s * CF::kAStage), b0 = dev::smem_u32(sB + s * CF::kBStage);
 #pragma unroll
-          for (int t = 0; t < kKSteps; ++t) {
-            const uint64_t bd = smem_desc(b0 + t * 2 * (CF::kNmma / 8) * 128, (CF::kNmma / 8) * 128, 128);
+            for (int tk = 0; tk < kKSteps; ++tk) {
+              const uint64_t bd = smem_desc(b0 + tk * 2 * (CF::kNmma / 8) * 128, (CF::kNmma / 8) * 128, 128);
 #pragma unroll
-            for (int i = 0; i < D; ++i) {
-              const uint64_t ad = smem_desc(a0 + i * (kBM * kBK) + t * 2 * (kBM / 8) * 128, (kBM / 8) * 128, 128);
-              mma_i8(tbase + i * CF::kNT, ad, bd, idesc, 1u);
+              for (int i = 0; i < D; ++i) {
+                const uint64_t ad = smem_desc(a0 + i * (kBM * kBK) + tk * 2 * (kBM / 8) * 128, (kBM / 8) * 128, 128);
+                mma_i8(tbase + i * NT, ad, bd, idesc, 1u);
+              }
             }
+            mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
           }
-          mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
+          mma_commit(tmem_full);    // this segment's accumulators are complete
         }
-        mma_commit(tmem_full);    // segment accumulators complete
       }
     }
   } else {
@@ -317,66 +354,87 @@ __global__ void __launch_bounds__(kThreads, 1) mwi8_kernel(const __grid_constant
     const int quad = warp % 4;                 // TMEM lane quadrant this warp may access
     const int row_in_tile = quad * 32 + lane;  // TMEM lane == tile row
     const uint32_t trow = tbase + (static_cast<uint32_t>(quad * 32) << 16);
-    const unsigned long long p = P.p, mu = P.mu;
-    constexpr int NT = CF::kNT;
-    const i64 row = static_cast<i64>(tm) * kBM + row_in_tile;
-    const i64 col_base = static_cast<i64>(tn) * NT;
-    double* dst_row = P.C + static_cast<i64>(blockIdx.y) * P.split_stride + row * P.ldc + col_base;
-    // zero the accumulators for the first segment
+    const unsigned long long p = P.p;
+    // this thread's scratch row: [block][NT] u32 (per-CTA region, L2 resident)
+    uint32_t* scr = P.scratch + (static_cast<i64>(blockIdx.x) * kBM + row_in_tile) * (NB_ * NT);
 #pragma unroll 1
-    for (int b = 0; b < CF::kBlocks; ++b)
+    for (int b = 0; b < NB_; ++b)
 #pragma unroll
       for (int c0 = 0; c0 < NT; c0 += 32) tmem_st32_zero(trow + b * NT + c0);
     tmem_wait_st();
     fence_before();
     __syncwarp();
     if (lane == 0) dev::mbar_arrive(tmem_empty);
-    for (int seg = 0; seg < nseg; ++seg) {
-      dev::mbar_wait(tmem_full, seg & 1);
-      fence_after();
-      // 32 output columns at a time: Horner over the weight blocks, top down
+    int e = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      const Item it = item_of(t, P);
+      const int kb0 = it.ks * P.kb_per_split;
+      const int nkb = max(0, min(P.KB, kb0 + P.kb_per_split) - kb0);
+      const int nseg = max(1, (nkb + P.seg_kb - 1) / P.seg_kb);
+      const i64 row = static_cast<i64>(it.tm) * kBM + row_in_tile;
+      const i64 col_base = static_cast<i64>(it.tn) * NT;
+      double* dst_row = P.C + static_cast<i64>(it.ks) * P.split_stride + row * P.ldc + col_base;
+      for (int seg = 0; seg < nseg; ++seg, ++e) {
+        dev::mbar_wait(tmem_full, e & 1);
+        fence_after();
+        // drain TMEM -> scratch, re-zero, hand the accumulators back
 #pragma unroll 1
-      for (int c0 = 0; c0 < NT; c0 += 32) {
-        unsigned long long h[32];
-        uint32_t v[32];
-        tmem_ld32(trow + (CF::kBlocks - 1) * NT + c0, v);
-        tmem_wait_ld();
-#pragma unroll
-        for (int c = 0; c < 32; ++c) h[c] = v[c] % p;
+        for (int b = 0; b < NB_; ++b) {
 #pragma unroll 1
-        for (int b = CF::kBlocks - 2; b >= 0; --b) {
-          tmem_ld32(trow + b * NT + c0, v);
-          tmem_wait_ld();
+          for (int c0 = 0; c0 < NT; c0 += 32) {
+            uint32_t v[32];
+            tmem_ld32(trow + b * NT + c0, v);
+            tmem_wait_ld();
+            uint4* d4 = reinterpret_cast<uint4*>(scr + b * NT + c0);
 #pragma unroll
-          for (int c = 0; c < 32; ++c) h[c] = barrett((h[c] << 8) + v[c], p, mu);
-        }
-        if (row < P.m) {
-          double* dst = dst_row + c0;
-          const i64 col0 = col_base + c0;
-          if (seg > 0) {  // earlier segments' residues were parked in C by this thread
-            for (int c = 0; c < 32 && col0 + c < P.n; ++c) {
-              const unsigned long long t = h[c] + static_cast<unsigned long long>(dst[c]);
-              h[c] = t >= p ? t - p : t;
-            }
-          }
-          if (col0 + 32 <= P.n && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-#pragma unroll
-            for (int c = 0; c < 32; c += 2)
-              *reinterpret_cast<double2*>(dst + c) = make_double2(static_cast<double>(h[c]), static_cast<double>(h[c + 1]));
-          } else {
-            for (int c = 0; c < 32 && col0 + c < P.n; ++c) dst[c] = static_cast<double>(h[c]);
+            for (int q = 0; q < 8; ++q) d4[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            tmem_st32_zero(trow + b * NT + c0);
           }
         }
-      }
-      if (seg + 1 < nseg) {  // re-zero and hand the accumulators back to the MMA warp
-#pragma unroll 1
-        for (int b = 0; b < CF::kBlocks; ++b)
-#pragma unroll
-          for (int c0 = 0; c0 < NT; c0 += 32) tmem_st32_zero(trow + b * NT + c0);
         tmem_wait_st();
         fence_before();
         __syncwarp();
         if (lane == 0) dev::mbar_arrive(tmem_empty);
+        // reconstruct sum_s 256^s T_s mod p while the MMAs of the next item run
+        if (row < P.m) {
+#pragma unroll 1
+          for (int c0 = 0; c0 < NT; c0 += 32) {
+            unsigned long long acc[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) acc[c] = 0;
+#pragma unroll 1
+            for (int b = 0; b < NB_; ++b) {
+              const uint4* s4 = reinterpret_cast<const uint4*>(scr + b * NT + c0);
+              const unsigned long long g = P.gam[b], gs = P.gam_sh[b];
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                const uint4 w = s4[q];
+                const uint32_t x[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                  const unsigned long long s2 = acc[4 * q + r] + shoup32(x[r], g, gs, p);
+                  acc[4 * q + r] = s2 >= p ? s2 - p : s2;
+                }
+              }
+            }
+            double* dst = dst_row + c0;
+            const i64 col0 = col_base + c0;
+            if (seg > 0) {  // earlier segments' residues were parked in C by this thread
+              for (int c = 0; c < 32 && col0 + c < P.n; ++c) {
+                const unsigned long long s2 = acc[c] + static_cast<unsigned long long>(dst[c]);
+                acc[c] = s2 >= p ? s2 - p : s2;
+              }
+            }
+            if (col0 + 32 <= P.n && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+#pragma unroll
+              for (int c = 0; c < 32; c += 2)
+                *reinterpret_cast<double2*>(dst + c) =
+                    make_double2(static_cast<double>(acc[c]), static_cast<double>(acc[c + 1]));
+            } else {
+              for (int c = 0; c < 32 && col0 + c < P.n; ++c) dst[c] = static_cast<double>(acc[c]);
+            }
+          }
+        }
       }
     }
   }
