@@ -1,0 +1,280 @@
+"""Command-line front end mirroring the reference's ``fpmm`` tool
+(/root/reference/proj/tools/fpmm_cli.cpp:92-169) for the B200 library:
+
+  python -m paper_2601_07508_b200.cli bench [--scenario square|unbalanced] [--dims m,k,n]
+        [--scale S] [--bits 20 26 ...] [--variant u,v|auto ...] [--lambda auto|N]
+        [--kernel b200|b200-i8|b200-dmma] [--runs R] [--seed S] [--out CSV] [--extended]
+  python -m paper_2601_07508_b200.cli crossover bench.csv [--out CSV]
+  python -m paper_2601_07508_b200.cli plan --bits B [--dims m,k,n] [--min-lambda L]
+
+``bench`` writes the reference's CSV schema v1 (bench.cpp:14-16, 35-45); with
+``--extended`` it appends engine, lambda_k, gpus and device-time columns.
+Timing follows run_bench (driver.cpp:222-243): for the square scenario the
+block size, both decompositions and the product are inside the timer; for
+the unbalanced scenario A's words are prepared once outside it.  Inputs are
+host matrices (the drop-in's calling convention), so the timer also covers
+the PCIe transfers.  ``crossover`` reproduces crossover_table
+(bench.cpp:93-136).  Exit codes follow the reference: 0 ok, 1 failure,
+2 usage error (fpmm_cli.cpp:14-16).
+"""
+from __future__ import annotations
+
+import argparse
+import csv
+import io
+import sys
+import time
+
+import numpy as np
+
+from . import (ENGINE_DMMA, ENGINE_I8, Error, FpContext, InfeasibleError, Timing, kVariants,
+               matrix_seed, mw_block_size, plan_for_modulus, prev_prime, random_mat,
+               variant_admits_bits)
+
+SCHEMA_VERSION = 1
+HEADER = ["schema_version", "scenario", "m", "k", "n", "bits", "p", "u", "v", "concat", "lambda",
+          "kernel", "runs", "t_avg_s", "eff_gflops", "status"]
+EXTENDED = ["engine", "lambda_k", "gpus", "device_ms"]
+KERNELS = {"b200": 0, "b200-i8": ENGINE_I8, "b200-dmma": ENGINE_DMMA}
+
+
+def preset_dims(scenario: str, scale: float):
+    """driver.cpp:142-157."""
+    def scaled(base, quantum, floor_to):
+        q = int(round(base * scale / quantum)) * quantum
+        return max(q, floor_to)
+    if scenario == "square":
+        n = scaled(10016, 32, 32)
+        return n, n, n
+    if scenario == "unbalanced":
+        return max(int(round(10923 * scale)), 1), scaled(32768, 32, 32), 32
+    raise Error("unknown scenario '%s' (square|unbalanced)" % scenario)
+
+
+def parse_dims(s: str):
+    parts = [int(x) for x in s.split(",")]
+    if len(parts) != 3 or min(parts) < 1:
+        raise Error("dims must be m,k,n with positive entries")
+    return tuple(parts)
+
+
+def parse_variants(vs):
+    if not vs or vs == ["auto"]:
+        return None
+    out = []
+    for v in vs:
+        u, w = (int(x) for x in v.split(","))
+        out.append((u, w))
+    return out
+
+
+def effective_gflops(m, k, n, t):
+    """bench.cpp:29-33."""
+    return 2.0 * m * k * n / t * 1e-9 if t > 0 else 0.0
+
+
+def run_bench(args) -> list:
+    m, k, n = parse_dims(args.dims) if args.dims else preset_dims(args.scenario, args.scale)
+    flags = KERNELS[args.kernel]
+    variants = parse_variants(args.variant)
+    rows = []
+    for bits in args.bits:
+        p = prev_prime(1 << bits) if bits <= 62 else 0
+        var_list = variants or [None]
+        for var in var_list:
+            rec = dict(schema_version=SCHEMA_VERSION, scenario=args.scenario, m=m, k=k, n=n, bits=bits,
+                       p=0, u=1, v=1, concat="none", kernel=args.kernel, runs=args.runs, t_avg_s=0.0,
+                       eff_gflops=0.0, status="ok", engine="", lambda_k=0, gpus=1, device_ms=0.0)
+            rec["lambda"] = 0
+            try:
+                if p < 5 or p.bit_length() != bits:
+                    raise InfeasibleError("no prime of this bitsize")
+                if var is None:
+                    pl = plan_for_modulus(p, m, k, n)
+                    u, v = pl.u, pl.v
+                else:
+                    u, v = var
+                    if bits > 52 or not variant_admits_bits(type(kVariants[0])(u, v), bits):
+                        raise InfeasibleError("variant does not admit this bitsize")
+                rec.update(p=p, u=u, v=v)
+                F = FpContext.make(p)
+                A = random_mat(m, k, p, matrix_seed(args.seed, bits, m, k, n, 0xA))
+                B = random_mat(k, n, p, matrix_seed(args.seed, bits, m, k, n, 0xB))
+                Cm = np.empty((m, n))
+                prepared = None
+                if args.scenario == "unbalanced":
+                    import torch
+                    from . import PreparedA
+                    prepared = PreparedA(torch.from_numpy(A).cuda(), p, u, v, flags=flags)
+                    dB = torch.empty((k, n), dtype=torch.float64, device="cuda")
+                    dC = torch.empty((m, n), dtype=torch.float64, device="cuda")
+                    hB = torch.from_numpy(B).pin_memory()
+                    hC = torch.empty((m, n), dtype=torch.float64).pin_memory()
+                total = dev = 0.0
+                lam_used = 0
+                for r in range(args.runs + 1):  # run 0 is an untimed warm-up (allocations)
+                    tm = Timing()
+                    t0 = time.perf_counter()
+                    lam = int(args.lambda_) if args.lambda_ != "auto" else min(mw_block_size(u, v, p) or 0, k)
+                    if lam < 1:
+                        raise InfeasibleError("block size infeasible")
+                    if prepared is None:
+                        from . import mw_product
+                        mw_product(A, B, u, v, lam, F, flags=flags, timing=tm, out=Cm)
+                    else:
+                        dB.copy_(hB, non_blocking=True)
+                        prepared.product(dB, dC, lam, timing=tm)
+                        hC.copy_(dC)
+                    dt = time.perf_counter() - t0
+                    if r > 0:
+                        total += dt
+                        dev += tm.total_ms
+                    lam_used = lam
+                rec["lambda"] = lam_used
+                rec["t_avg_s"] = total / args.runs
+                rec["eff_gflops"] = effective_gflops(m, k, n, rec["t_avg_s"])
+                rec["engine"] = "i8" if (flags or ENGINE_I8) & ENGINE_I8 else "dmma"
+                rec["lambda_k"] = tm.lambda_k
+                rec["device_ms"] = dev / args.runs
+                if prepared is not None:
+                    prepared.close()
+            except InfeasibleError:
+                rec["status"] = "infeasible"
+            rows.append(rec)
+    return rows
+
+
+def write_csv(rows, out, extended=False):
+    cols = HEADER + (EXTENDED if extended else [])
+    w = csv.writer(out, lineterminator="\n")
+    w.writerow(cols)
+    for r in rows:
+        vals = []
+        for c in cols:
+            x = r[c]
+            if c == "t_avg_s":
+                x = "%.9g" % x
+            elif c == "eff_gflops":
+                x = "%.6g" % x
+            elif c == "device_ms":
+                x = "%.6g" % x
+            vals.append(x)
+        w.writerow(vals)
+
+
+def read_csv(path):
+    with open(path) as f:
+        rd = csv.reader(f)
+        head = next(rd, None)
+        if head is None:
+            raise Error("bench csv: empty input")
+        if head[:16] != HEADER:
+            raise Error("bench csv: unrecognized header/schema: '%s'" % ",".join(head))
+        rows = []
+        for line in rd:
+            if not line:
+                continue
+            r = dict(zip(head, line))
+            rows.append(dict(bits=int(r["bits"]), u=int(r["u"]), v=int(r["v"]),
+                             eff_gflops=float(r["eff_gflops"]), status=r["status"]))
+        return rows
+
+
+def crossover_table(rows):
+    """bench.cpp:93-136: per-bitsize winner merged into segments."""
+    best, seen_bits, seen_var = {}, set(), set()
+    for r in rows:
+        seen_bits.add(r["bits"])
+        if r["status"] != "ok":
+            continue
+        seen_var.add((r["u"], r["v"]))
+        w = best.get(r["bits"])
+        if w is None:
+            best[r["bits"]] = r
+            continue
+        uv, wuv = r["u"] * r["v"], w["u"] * w["v"]
+        if r["eff_gflops"] > w["eff_gflops"] or (
+                r["eff_gflops"] == w["eff_gflops"] and
+                (uv < wuv or (uv == wuv and (r["u"] + r["v"] < w["u"] + w["v"] or
+                                            (r["u"] + r["v"] == w["u"] + w["v"] and r["u"] < w["u"]))))):
+            best[r["bits"]] = r
+    if len(seen_var) < 2:
+        raise Error("crossover: need measurements for at least two variants")
+    if not seen_bits:
+        raise Error("crossover: no rows")
+    lo, hi = min(seen_bits), max(seen_bits)
+    missing = [b for b in range(lo, hi + 1) if b not in seen_bits]
+    if missing:
+        raise Error("crossover: sweep has gaps at bitsizes " + ", ".join(map(str, missing)))
+    out = []
+    for b in range(lo, hi + 1):
+        w = best.get(b)
+        if w is None:
+            continue
+        var = (w["u"], w["v"])
+        if out and out[-1][0] == var and out[-1][2] == b - 1:
+            out[-1][2] = b
+        else:
+            out.append([var, b, b])
+    return out
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser(prog="fpmm-b200", description="exact modular matrix multiplication on B200")
+    sub = ap.add_subparsers(dest="cmd", required=True)
+    b = sub.add_parser("bench", help="measure effective Gflops/s, emit CSV")
+    b.add_argument("--scenario", default="square", choices=["square", "unbalanced"])
+    b.add_argument("--dims")
+    b.add_argument("--scale", type=float, default=1.0)
+    b.add_argument("--bits", type=int, nargs="+", default=list(range(20, 53)))
+    b.add_argument("--variant", nargs="+", default=["auto"])
+    b.add_argument("--lambda", dest="lambda_", default="auto")
+    b.add_argument("--kernel", default="b200", choices=sorted(KERNELS))
+    b.add_argument("--runs", type=int, default=10)
+    b.add_argument("--seed", type=int, default=1)
+    b.add_argument("--out")
+    b.add_argument("--extended", action="store_true")
+    c = sub.add_parser("crossover", help="best-variant bitsize intervals from a bench CSV")
+    c.add_argument("csv")
+    c.add_argument("--out")
+    pl = sub.add_parser("plan", help="variant/block-size plan for a bitsize and shape")
+    pl.add_argument("--bits", type=int, required=True)
+    pl.add_argument("--dims", default="1024,1024,1024")
+    pl.add_argument("--min-lambda", type=int, default=1)
+    try:
+        args = ap.parse_args(argv)
+    except SystemExit as e:
+        return 2 if e.code else 0
+    try:
+        if args.cmd == "bench":
+            rows = run_bench(args)
+            if args.out:
+                with open(args.out, "w") as f:
+                    write_csv(rows, f, args.extended)
+            else:
+                write_csv(rows, sys.stdout, args.extended)
+        elif args.cmd == "crossover":
+            table = crossover_table(read_csv(args.csv))
+            buf = io.StringIO()
+            buf.write("u,v,best_bits_lo,best_bits_hi\n")
+            for (u, v), lo, hi in table:
+                buf.write("%d,%d,%d,%d\n" % (u, v, lo, hi))
+            if args.out:
+                open(args.out, "w").write(buf.getvalue())
+            else:
+                sys.stdout.write(buf.getvalue())
+        else:
+            from . import select_variant
+            m, k, n = parse_dims(args.dims)
+            p = select_variant(args.bits, m, k, n, min_lambda=args.min_lambda)
+            print("bits=%d dims=%d,%d,%d variant=(%d,%d) lambda=%d concat=%s products=%d reductions=%d "
+                  "storage=%d" % (args.bits, m, k, n, p.u, p.v, p.lambda_, p.concat, p.predicted_products,
+                                  p.predicted_reductions, p.storage_entries))
+    except Error as e:
+        print("error: %s" % e, file=sys.stderr)
+        return 1
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

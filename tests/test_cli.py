@@ -1,0 +1,52 @@
+"""CLI parity (fpmm_cli.cpp): plan output, CSV schema v1, crossover table."""
+import io
+
+import pytest
+
+from paper_2601_07508_b200 import cli
+
+
+def test_plan_and_usage(capsys):
+    assert cli.main(["plan", "--bits", "37"]) == 0
+    assert "variant=(1,3)" in capsys.readouterr().out
+    assert cli.main(["plan", "--bits", "53"]) == 1
+    assert cli.main(["frobnicate"]) == 2
+
+
+def test_preset_dims():
+    assert cli.preset_dims("square", 1.0) == (10016, 10016, 10016)
+    assert cli.preset_dims("unbalanced", 1.0) == (10923, 32768, 32)
+    assert cli.preset_dims("square", 0.1) == (992, 992, 992)  # llround(1001.6/32)*32
+
+
+def test_crossover_from_csv(tmp_path):
+    rows = []
+    for bits in range(20, 30):
+        for (u, v), g in (((1, 1), 100 - 5 * max(0, bits - 24)), ((1, 2), 60)):
+            rows.append(dict(schema_version=1, scenario="square", m=8, k=8, n=8, bits=bits, p=0, u=u, v=v,
+                             concat="none", kernel="b200", runs=1, t_avg_s=1.0, eff_gflops=float(g),
+                             status="ok" if (u, v) == (1, 2) or bits <= 26 else "infeasible", **{"lambda": 1}))
+    path = tmp_path / "b.csv"
+    with open(path, "w") as f:
+        cli.write_csv(rows, f)
+    head = open(path).readline().strip()
+    assert head == ",".join(cli.HEADER)
+    table = cli.crossover_table(cli.read_csv(str(path)))
+    assert table == [[(1, 1), 20, 26], [(1, 2), 27, 29]]
+    with pytest.raises(cli.Error):
+        cli.crossover_table([r for r in cli.read_csv(str(path)) if r["bits"] != 23])
+
+
+@pytest.mark.gpu
+def test_bench_csv_on_gpu(tmp_path):
+    out = tmp_path / "bench.csv"
+    assert cli.main(["bench", "--dims", "256,256,256", "--bits", "20", "26", "27", "--variant", "1,1", "1,2",
+                     "--runs", "2", "--out", str(out), "--extended"]) == 0
+    lines = open(out).read().strip().split("\n")
+    assert lines[0].startswith(",".join(cli.HEADER))
+    body = [l.split(",") for l in lines[1:]]
+    assert len(body) == 6
+    status = {(int(r[5]), int(r[7]), int(r[8])): r[15] for r in body}
+    assert status[(27, 1, 1)] == "infeasible" and status[(26, 1, 1)] == "ok"
+    assert cli.main(["bench", "--scenario", "unbalanced", "--scale", "0.05", "--bits", "40", "--runs", "1",
+                     "--out", str(tmp_path / "u.csv")]) == 0
