@@ -328,6 +328,11 @@ void launch_gemm_i8(const Job& j, const void* apack, const void* bpack, double* 
     const i64 want = (2 * 148 + tiles0 - 1) / tiles0;
     splits = static_cast<int>(std::max<i64>(1, std::min<i64>({want, j.KB / 16, 32})));
   }
+  // Long K: one split per exact int32 segment, slices ordered split-major, so
+  // every wave of 148 items streams one K-chunk of its panels (~100 MB at
+  // D=7) instead of the whole K (measured at 8192 x 32768 x 8192: L2 hit rate
+  // 52% and 222 GB of DRAM reads with in-item segments).
+  if (j.KB > q.seg_kb) splits = std::max<int>(splits, (j.KB + q.seg_kb - 1) / q.seg_kb);
   q.kb_per_split = (j.KB + splits - 1) / splits;
   splits = (j.KB + q.kb_per_split - 1) / q.kb_per_split;
   q.splits = splits;
@@ -346,8 +351,6 @@ void launch_gemm_i8(const Job& j, const void* apack, const void* bpack, double* 
   CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const i64 items = static_cast<i64>(q.MB) * q.NB * splits;
   const unsigned grid = static_cast<unsigned>(std::max<i64>(1, std::min<i64>(items, sms)));
-  q.scratch = static_cast<uint32_t*>(
-      dc.scratch.get(sizeof(uint32_t) * static_cast<size_t>(grid) * i8::kBM * (2 * j.D - 1) * j.BN));
   dispatch_d(j.D, [&]<int D>() {
     using CF = i8::Cfg<D>;
     auto kern = i8::mwi8_kernel<D>;

@@ -144,7 +144,6 @@ struct Params {
   i64 split_stride;     // split-K: C offset (elements) between the slices' partial outputs
   unsigned long long p, mu;
   unsigned long long gam[13], gam_sh[13];  // 256^s mod p and Shoup constants, s = 0 .. 2D-2
-  uint32_t* scratch;    // per-CTA TMEM drain area: gridDim.x x 128 x (2D-1) NT u32
 };
 
 // --------------------------------------------------------------- packing
@@ -254,11 +253,9 @@ __device__ __forceinline__ uint64_t shoup32(uint32_t x, uint64_t g, uint64_t gs,
   return r >= p ? r - p : r;
 }
 
-// Persistent: one CTA per SM loops over work items.  TMEM holds one set of
-// 2D-1 weight blocks; the epilogue drains it to a per-CTA L2-resident scratch
-// (a few microseconds), re-zeroes it and releases it to the MMA warp, then
-// reconstructs C = sum_s 256^s T_s mod p from the scratch while the tensor
-// cores already run the next item.
+// Persistent: one CTA per SM loops over work items (TMEM allocation, barrier
+// set-up and the pipeline fill are paid once per SM, and the TMA producer
+// runs ahead into the next item while the epilogue reconstructs the last).
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1) mwi8_kernel(const __grid_constant__ Params P) {
   using CF = Cfg<D>;
@@ -351,12 +348,16 @@ __global__ void __launch_bounds__(kThreads, 1) mwi8_kernel(const __grid_constant
     }
   } else {
     // ---------------- epilogue: warps 2..5 ----------------
+    // Reconstruct straight from TMEM: sum_s (256^s mod p) T_s with Shoup
+    // products (independent terms, no Horner chain), re-zero each block as it
+    // is consumed, release the accumulators, then store C.  (Draining TMEM to
+    // an L2 scratch to overlap this with the next item's MMAs was measured
+    // slower: the 208 KB/item scratch traffic cost more power than the
+    // overlap won on this power-capped part.)
     const int quad = warp % 4;                 // TMEM lane quadrant this warp may access
     const int row_in_tile = quad * 32 + lane;  // TMEM lane == tile row
     const uint32_t trow = tbase + (static_cast<uint32_t>(quad * 32) << 16);
     const unsigned long long p = P.p;
-    // this thread's scratch row: [block][NT] u32 (per-CTA region, L2 resident)
-    uint32_t* scr = P.scratch + (static_cast<i64>(blockIdx.x) * kBM + row_in_tile) * (NB_ * NT);
 #pragma unroll 1
     for (int b = 0; b < NB_; ++b)
 #pragma unroll
@@ -377,46 +378,31 @@ __global__ void __launch_bounds__(kThreads, 1) mwi8_kernel(const __grid_constant
       for (int seg = 0; seg < nseg; ++seg, ++e) {
         dev::mbar_wait(tmem_full, e & 1);
         fence_after();
-        // drain TMEM -> scratch, re-zero, hand the accumulators back
 #pragma unroll 1
-        for (int b = 0; b < NB_; ++b) {
+        for (int c0 = 0; c0 < NT; c0 += 32) {
+          unsigned long long acc[32];
+#pragma unroll
+          for (int c = 0; c < 32; ++c) acc[c] = 0;
 #pragma unroll 1
-          for (int c0 = 0; c0 < NT; c0 += 32) {
+          for (int b = 0; b < NB_; ++b) {
             uint32_t v[32];
             tmem_ld32(trow + b * NT + c0, v);
             tmem_wait_ld();
-            uint4* d4 = reinterpret_cast<uint4*>(scr + b * NT + c0);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) d4[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
             tmem_st32_zero(trow + b * NT + c0);
-          }
-        }
-        tmem_wait_st();
-        fence_before();
-        __syncwarp();
-        if (lane == 0) dev::mbar_arrive(tmem_empty);
-        // reconstruct sum_s 256^s T_s mod p while the MMAs of the next item run
-        if (row < P.m) {
-#pragma unroll 1
-          for (int c0 = 0; c0 < NT; c0 += 32) {
-            unsigned long long acc[32];
+            const unsigned long long g = P.gam[b], gs = P.gam_sh[b];
 #pragma unroll
-            for (int c = 0; c < 32; ++c) acc[c] = 0;
-#pragma unroll 1
-            for (int b = 0; b < NB_; ++b) {
-              const uint4* s4 = reinterpret_cast<const uint4*>(scr + b * NT + c0);
-              const unsigned long long g = P.gam[b], gs = P.gam_sh[b];
-#pragma unroll
-              for (int q = 0; q < 8; ++q) {
-                const uint4 w = s4[q];
-                const uint32_t x[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                  const unsigned long long s2 = acc[4 * q + r] + shoup32(x[r], g, gs, p);
-                  acc[4 * q + r] = s2 >= p ? s2 - p : s2;
-                }
-              }
+            for (int c = 0; c < 32; ++c) {
+              const unsigned long long s2 = acc[c] + shoup32(v[c], g, gs, p);
+              acc[c] = s2 >= p ? s2 - p : s2;
             }
+          }
+          if (c0 + 32 >= NT) {  // every block consumed and re-zeroed: release TMEM
+            tmem_wait_st();
+            fence_before();
+            __syncwarp();
+            if (lane == 0) dev::mbar_arrive(tmem_empty);
+          }
+          if (row < P.m) {
             double* dst = dst_row + c0;
             const i64 col0 = col_base + c0;
             if (seg > 0) {  // earlier segments' residues were parked in C by this thread
