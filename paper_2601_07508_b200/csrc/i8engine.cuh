@@ -172,10 +172,21 @@ __global__ void __launch_bounds__(256) pack_a_i8(const double* __restrict__ A, i
     for (int i = 0; i < D; ++i) w[i][0] = w[i][1] = w[i][2] = w[i][3] = 0;
     if (row < m) {
       const double* src = A + row * lda + kc * 16;
+      double xs[16];
+      if (kc * 16 + 16 <= k && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+#pragma unroll
+        for (int e = 0; e < 16; e += 2) {  // 16-byte loads
+          const double2 t = __ldg(reinterpret_cast<const double2*>(src + e));
+          xs[e] = t.x;
+          xs[e + 1] = t.y;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) xs[e] = kc * 16 + e < k ? src[e] : 0.0;
+      }
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
-        const i64 col = kc * 16 + e;
-        const unsigned long long x = col < k ? static_cast<unsigned long long>(src[e]) : 0ull;
+        const unsigned long long x = static_cast<unsigned long long>(xs[e]);
 #pragma unroll
         for (int i = 0; i < D; ++i) w[i][e / 4] |= static_cast<uint32_t>((x >> (8 * i)) & 0xFF) << (8 * (e % 4));
       }
@@ -213,7 +224,9 @@ __global__ void __launch_bounds__(256) pack_b_i8(const double* __restrict__ B, i
     uint8_t* base = out + (cb * KB + kb) * static_cast<i64>(Cfg<D>::kBStage);
     // units: (digit j, column cc, k16 chunk q): 16 bytes each
     for (int u = threadIdx.x; u < D * 32 * (kBK / 16); u += blockDim.x) {
-      const int q = u % (kBK / 16), cc = (u / (kBK / 16)) % 32, j = u / ((kBK / 16) * 32);
+      // lanes walk the 32 columns: 2-way (64-bit) bank access, and 32
+      // consecutive 16-byte rows of one core-matrix column -> 512 B stores
+      const int cc = u % 32, q = (u / 32) % (kBK / 16), j = u / ((kBK / 16) * 32);
       uint32_t w[4] = {0, 0, 0, 0};
 #pragma unroll
       for (int e = 0; e < 16; ++e)
