@@ -59,7 +59,7 @@ struct DevBuf {
 };
 
 struct DeviceCtx {
-  static constexpr int kChunks = 8;  // host-path pipeline depth
+  static constexpr int kChunks = 16;  // host-path pipeline depth (exposed head/tail ~1/16 of a product)
   int dev = -1;
   cudaStream_t stream = nullptr, s_in = nullptr, s_out = nullptr;
   cudaEvent_t ev[8] = {}, ev_in[kChunks] = {}, ev_out[kChunks] = {};

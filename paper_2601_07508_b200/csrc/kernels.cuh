@@ -116,8 +116,12 @@ __global__ void __launch_bounds__(256) pack_b_kernel(const double* __restrict__ 
   const i64 np2 = npad / 2, total = np2 * KB * 16;
   for (i64 idx = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
        idx += static_cast<i64>(gridDim.x) * blockDim.x) {
-    const i64 t = idx % np2, c = idx / np2;  // column pair, k row
-    const i64 n0 = (t / 8) * 16 + (t % 8), n1 = n0 + 8;
+    // a warp covers 8 column pairs x 4 k rows = one fragment's 32 lanes, so
+    // its 16-byte stores form one contiguous 512-byte run
+    const int c4 = static_cast<int>(idx % 4), nn = static_cast<int>((idx / 4) % 8);
+    const i64 rest = idx / 32, g16 = rest % (np2 / 8), kq = rest / (np2 / 8);
+    const i64 c = kq * 4 + c4;                   // k row
+    const i64 n0 = g16 * 16 + nn, n1 = n0 + 8;   // column pair
     double v0 = 0.0, v1 = 0.0;
     if (c < k) {
       if (n0 < n) v0 = B[c * ldb + n0];
@@ -193,7 +197,7 @@ __global__ void __launch_bounds__(256, 1) mwgemm_kernel(const __grid_constant__ 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       dev::mbar_init(&full[s], 1);
-      dev::mbar_init(&empty[s], Cfg::kWarps);
+      dev::mbar_init(&empty[s], Cfg::kThreads);  // every consumer thread releases its own reads
     }
     dev::fence_barrier_init();
   }
@@ -266,8 +270,7 @@ __global__ void __launch_bounds__(256, 1) mwgemm_kernel(const __grid_constant__ 
               }
       }
     }
-    __syncwarp();
-    if (lane == 0) dev::mbar_arrive(&empty[s]);
+    dev::mbar_arrive(&empty[s]);  // release: this thread's LDS reads of stage s are done
     // refill the stage consumed in the previous iteration (its empty barrier
     // is normally complete by now, so the producer rarely waits)
     if (tid == 0 && it >= 1) {
