@@ -222,6 +222,10 @@ int fpmm_b200_fp64_peak(int device, int iters, double* tflops);
 /* Measured int8 tensor-core peak (TOP/s): back-to-back tcgen05.mma.kind::i8
  * M=128 N=256 K=32 on every SM. */
 int fpmm_b200_i8_peak(int device, int iters, double* tops);
+/* Diagnostic tensor-pipe probe: mode 0 = one CTA per SM (M128 N256), mode 1 =
+ * CTA pairs issuing cta_group::2 M256 N256 MMAs.  Long `iters` measure the
+ * sustained (power-capped) rate. */
+int fpmm_b200_i8_probe(int device, int iters, int mode, double* tops);
 
 /* release every device workspace, stream and communicator */
 int fpmm_b200_finalize(void);

@@ -265,6 +265,10 @@ int fpmm_b200_i8_peak(int device, int iters, double* tops) {
   return guarded([&] { *tops = i8_peak_tops(device, iters); });
 }
 
+int fpmm_b200_i8_probe(int device, int iters, int mode, double* tops) {
+  return guarded([&] { *tops = i8_probe_tops(device, iters, mode); });
+}
+
 int fpmm_b200_finalize(void) {
   return guarded([&] { finalize_all(); });
 }

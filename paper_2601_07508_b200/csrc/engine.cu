@@ -914,6 +914,29 @@ double fp64_peak_tflops(int device, int iters) {
   return flops / (ms * 1e-3) / 1e12;
 }
 
+double i8_probe_tops(int device, int iters, int mode) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  DeviceCtx& c = ctx(device);
+  int sms = 0;
+  CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  int* out = static_cast<int*>(c.err.get(4096));
+  const int grid = mode == 1 ? (sms / 2) * 2 : sms;
+  auto launch = [&](int it) {
+    if (mode == 1) i8::i8_peak2_kernel<<<grid, 64, 0, c.stream>>>(it, out);
+    else i8::i8_peak_kernel<<<grid, 64, 0, c.stream>>>(it, out);
+  };
+  launch(iters / 8);
+  CUDA_OK(cudaEventRecord(c.ev[0], c.stream));
+  launch(iters);
+  CUDA_OK(cudaEventRecord(c.ev[1], c.stream));
+  CUDA_OK(cudaEventSynchronize(c.ev[1]));
+  CUDA_OK(cudaGetLastError());
+  const double ms = elapsed(c.ev[0], c.ev[1]);
+  // per MMA: 1-CTA M128 N256 K32 on every SM; 2-CTA M256 N256 K32 per pair
+  const double ops = mode == 1 ? 2.0 * 256 * 256 * 32 * iters * (grid / 2) : 2.0 * i8::kBM * 256.0 * 32.0 * iters * grid;
+  return ops / (ms * 1e-3) / 1e12;
+}
+
 double i8_peak_tops(int device, int iters) {
   std::lock_guard<std::recursive_mutex> lk(g_mu);
   DeviceCtx& c = ctx(device);

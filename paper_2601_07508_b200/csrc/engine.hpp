@@ -58,6 +58,7 @@ void random_residues_device(double* dM, i64 ld, i64 rows, i64 cols, i64 row0, u6
                             void* stream);
 double fp64_peak_tflops(int device, int iters);
 double i8_peak_tops(int device, int iters);
+double i8_probe_tops(int device, int iters, int mode);
 void finalize_all();
 
 // multi-process partitioner

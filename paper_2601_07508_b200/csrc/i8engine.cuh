@@ -466,8 +466,9 @@ __global__ void __launch_bounds__(64, 1) i8_peak_kernel(int iters, int* out) {
   __shared__ uint64_t done;
   __shared__ uint32_t slot;
   const int warp = threadIdx.x / 32;
+  // random operand bytes: realistic toggling (zero operands draw ~1/3 of the power)
   for (int e = threadIdx.x; e < static_cast<int>(sizeof(ops)) / 4; e += blockDim.x)
-    reinterpret_cast<uint32_t*>(ops)[e] = 0;
+    reinterpret_cast<uint32_t*>(ops)[e] = static_cast<uint32_t>(e * 2654435761u + blockIdx.x * 40503u) ^ 0x5bd1e995u;
   if (threadIdx.x == 0) {
     dev::mbar_init(&done, 1);
     dev::fence_barrier_init();
@@ -498,6 +499,77 @@ __global__ void __launch_bounds__(64, 1) i8_peak_kernel(int iters, int* out) {
     tmem_wait_ld();
     if (v[0] == 12345u) out[0] = 1;
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tbase));
+  }
+}
+
+// ---- cta_group::2 probe: a CTA pair (cluster of 2) issues M=256 N=256 K=32
+// kind::i8 MMAs from the leader; each CTA holds its 128-row A half and half
+// of B.  Used to measure the pair's sustained rate against the 1-CTA probe.
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void mma_i8_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  const uint32_t z = 0;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(z));
+}
+__device__ __forceinline__ void mma_commit_2sm(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+          dev::smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64, 1) i8_peak2_kernel(int iters, int* out) {
+  __shared__ __align__(1024) uint8_t ops[kBM * 32 + 128 * 32];  // A half (128x32) + B half (128 rows x 32)
+  __shared__ uint64_t done;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x / 32;
+  const uint32_t rank = cluster_rank();
+  for (int e = threadIdx.x; e < static_cast<int>(sizeof(ops)) / 4; e += blockDim.x)
+    reinterpret_cast<uint32_t*>(ops)[e] = static_cast<uint32_t>(e * 2654435761u + blockIdx.x * 40503u) ^ 0x5bd1e995u;
+  if (threadIdx.x == 0) {
+    dev::mbar_init(&done, 1);
+    dev::fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(dev::smem_u32(&slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  fence_before();
+  cluster_sync_all();
+  fence_after();
+  const uint32_t tbase = slot;
+  if (rank == 0 && threadIdx.x == 0) {
+    const uint32_t a = dev::smem_u32(ops), b = a + kBM * 32;
+    const uint64_t ad = smem_desc(a, (kBM / 8) * 128, 128), bd = smem_desc(b, (128 / 8) * 128, 128);
+    constexpr uint32_t idesc = instr_desc(256, 256);
+    for (int it = 0; it < iters; ++it) mma_i8_2sm(tbase, ad, bd, idesc, it > 0 ? 1u : 0u);
+    mma_commit_2sm(&done, 0x3);
+  }
+  if (threadIdx.x == 0) dev::mbar_wait(&done, 0);
+  fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    fence_after();
+    uint32_t v[32];
+    tmem_ld32(tbase + (32u << 16), v);
+    tmem_wait_ld();
+    if (v[0] == 12345u) out[0] = 1;
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 256;\n" ::"r"(tbase));
   }
 }
 
