@@ -34,13 +34,13 @@ constexpr int kBK = 64;       // k bytes (int8 elements) per pipeline stage
 constexpr int kKSteps = kBK / 32;  // MMA K = 32 for kind::i8
 constexpr int kThreads = 192;      // 6 warps
 
-// Output columns per CTA tile (NT): the widest multiple of 32 with
-// (2D-1) NT <= 512 TMEM columns and N_mma = D NT <= 256.  Wider tiles read
+// Output columns per CTA tile (NT): the widest NT (a multiple of 8) with
+// (2D-1) NT <= 512 TMEM columns and N_mma = D NT <= 256, N_mma % 16 == 0.  Wider tiles read
 // less shared memory per MMA (A is re-read once per MMA) and amortise the
 // per-tile epilogue over more work.
 template <int D>
 struct Cfg {
-  static constexpr int kNT = D == 1 ? 256 : D == 2 ? 128 : D <= 4 ? 64 : 32;
+  static constexpr int kNT = D == 1 ? 256 : D == 2 ? 128 : D <= 4 ? 64 : D == 5 ? 48 : D == 6 ? 40 : 32;
   static constexpr int kAStage = D * kBM * kBK;        // bytes: D digit tiles of 128 x 64
   static constexpr int kBStage = D * kNT * kBK;        // bytes: B_cat tile of (NT D) x 64
   static constexpr int kStageBytes = kAStage + kBStage;
@@ -119,6 +119,54 @@ __device__ __forceinline__ void tmem_st32_zero(uint32_t taddr) {
       "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};\n" ::"r"(taddr),
       "r"(z)
       : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st16_zero(uint32_t taddr) {
+  const uint32_t z = 0;
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};\n" ::"r"(
+                   taddr),
+               "r"(z)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_st8_zero(uint32_t taddr) {
+  const uint32_t z = 0;
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};\n" ::"r"(taddr), "r"(z)
+               : "memory");
+}
+template <int W>
+__device__ __forceinline__ void tmem_ldw(uint32_t taddr, uint32_t* r) {
+  if constexpr (W == 32) tmem_ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(r));
+  else if constexpr (W == 16) tmem_ld16(taddr, r);
+  else tmem_ld8(taddr, r);
+}
+template <int W>
+__device__ __forceinline__ void tmem_zerow(uint32_t taddr) {
+  if constexpr (W == 32) tmem_st32_zero(taddr);
+  else if constexpr (W == 16) tmem_st16_zero(taddr);
+  else tmem_st8_zero(taddr);
+}
+// zero every TMEM column of the 2D-1 blocks this lane quadrant owns
+template <int NBLK, int NT>
+__device__ __forceinline__ void tmem_zero_all(uint32_t trow) {
+  constexpr int FULL = NT - NT % 32;
+#pragma unroll 1
+  for (int b = 0; b < NBLK; ++b) {
+#pragma unroll
+    for (int c0 = 0; c0 < FULL; c0 += 32) tmem_st32_zero(trow + b * NT + c0);
+    if constexpr (NT % 32 != 0) tmem_zerow<NT % 32>(trow + b * NT + FULL);
+  }
 }
 
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
@@ -208,30 +256,32 @@ __global__ void __launch_bounds__(256) pack_a_i8(const double* __restrict__ A, i
 template <int D>
 __global__ void __launch_bounds__(256) pack_b_i8(const double* __restrict__ B, i64 ldb, i64 k, i64 n,
                                                  int KB, int NB, uint8_t* __restrict__ out) {
-  constexpr int NT = Cfg<D>::kNT, SUB = NT / 32;
-  __shared__ unsigned long long tile[kBK][33];
+  constexpr int NT = Cfg<D>::kNT;
+  constexpr int SW = NT % 32 == 0 ? 32 : NT % 16 == 0 ? 16 : 8;  // sub-block columns
+  constexpr int SUB = NT / SW;
+  __shared__ unsigned long long tile[kBK][SW + 1];
   const i64 tiles = static_cast<i64>(KB) * NB * SUB;
   for (i64 t = blockIdx.x; t < tiles; t += gridDim.x) {
     const int sb = static_cast<int>(t % SUB);
     const i64 cb = (t / SUB) % NB, kb = t / (SUB * static_cast<i64>(NB));
     __syncthreads();
-    for (int e = threadIdx.x; e < kBK * 32; e += blockDim.x) {
-      const int kr = e / 32, cc = e % 32;
-      const i64 kk = kb * kBK + kr, col = cb * NT + sb * 32 + cc;
+    for (int e = threadIdx.x; e < kBK * SW; e += blockDim.x) {
+      const int kr = e / SW, cc = e % SW;
+      const i64 kk = kb * kBK + kr, col = cb * NT + sb * SW + cc;
       tile[kr][cc] = (kk < k && col < n) ? static_cast<unsigned long long>(B[kk * ldb + col]) : 0ull;
     }
     __syncthreads();
     uint8_t* base = out + (cb * KB + kb) * static_cast<i64>(Cfg<D>::kBStage);
     // units: (digit j, column cc, k16 chunk q): 16 bytes each
-    for (int u = threadIdx.x; u < D * 32 * (kBK / 16); u += blockDim.x) {
+    for (int u = threadIdx.x; u < D * SW * (kBK / 16); u += blockDim.x) {
       // lanes walk the 32 columns: 2-way (64-bit) bank access, and 32
       // consecutive 16-byte rows of one core-matrix column -> 512 B stores
-      const int cc = u % 32, q = (u / 32) % (kBK / 16), j = u / ((kBK / 16) * 32);
+      const int cc = u % SW, q = (u / SW) % (kBK / 16), j = u / ((kBK / 16) * SW);
       uint32_t w[4] = {0, 0, 0, 0};
 #pragma unroll
       for (int e = 0; e < 16; ++e)
         w[e / 4] |= static_cast<uint32_t>((tile[q * 16 + e][cc] >> (8 * j)) & 0xFF) << (8 * (e % 4));
-      const int nn = j * NT + sb * 32 + cc, g = nn / 8, r8 = nn % 8;
+      const int nn = j * NT + sb * SW + cc, g = nn / 8, r8 = nn % 8;
       *reinterpret_cast<uint4*>(base + ((q * (D * NT / 8) + g) * 8 + r8) * 16) = make_uint4(w[0], w[1], w[2], w[3]);
     }
   }
@@ -264,6 +314,54 @@ __device__ __forceinline__ uint64_t shoup32(uint32_t x, uint64_t g, uint64_t gs,
   const uint64_t q = __umul64hi(static_cast<uint64_t>(x), gs);
   const uint64_t r = static_cast<uint64_t>(x) * g - q * p;
   return r >= p ? r - p : r;
+}
+
+// One W-column chunk of the epilogue: sum_s (256^s mod p) T_s over the
+// weight blocks (re-zeroing each as it is read), optional release of TMEM,
+// then the C store (read-modify-write when earlier K segments were parked).
+template <int W, int NBLK, int NT>
+__device__ __forceinline__ void epi_chunk(const Params& P, uint32_t trow, int c0, bool last, uint64_t* tmem_empty,
+                                          int lane, int seg, i64 row, i64 col_base, double* dst_row) {
+  const unsigned long long p = P.p;
+  unsigned long long acc[W];
+#pragma unroll
+  for (int c = 0; c < W; ++c) acc[c] = 0;
+#pragma unroll 1
+  for (int b = 0; b < NBLK; ++b) {
+    uint32_t v[W];
+    tmem_ldw<W>(trow + b * NT + c0, v);
+    tmem_wait_ld();
+    tmem_zerow<W>(trow + b * NT + c0);
+    const unsigned long long g = P.gam[b], gs = P.gam_sh[b];
+#pragma unroll
+    for (int c = 0; c < W; ++c) {
+      const unsigned long long s2 = acc[c] + shoup32(v[c], g, gs, p);
+      acc[c] = s2 >= p ? s2 - p : s2;
+    }
+  }
+  if (last) {  // every block consumed and re-zeroed: release TMEM to the MMA warp
+    tmem_wait_st();
+    fence_before();
+    __syncwarp();
+    if (lane == 0) dev::mbar_arrive(tmem_empty);
+  }
+  if (row < P.m) {
+    double* dst = dst_row + c0;
+    const i64 col0 = col_base + c0;
+    if (seg > 0) {  // earlier segments' residues were parked in C by this thread
+      for (int c = 0; c < W && col0 + c < P.n; ++c) {
+        const unsigned long long s2 = acc[c] + static_cast<unsigned long long>(dst[c]);
+        acc[c] = s2 >= p ? s2 - p : s2;
+      }
+    }
+    if (col0 + W <= P.n && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+#pragma unroll
+      for (int c = 0; c < W; c += 2)
+        *reinterpret_cast<double2*>(dst + c) = make_double2(static_cast<double>(acc[c]), static_cast<double>(acc[c + 1]));
+    } else {
+      for (int c = 0; c < W && col0 + c < P.n; ++c) dst[c] = static_cast<double>(acc[c]);
+    }
+  }
 }
 
 // Persistent: one CTA per SM loops over work items (TMEM allocation, barrier
@@ -370,15 +468,12 @@ __global__ void __launch_bounds__(kThreads, 1) mwi8_kernel(const __grid_constant
     const int quad = warp % 4;                 // TMEM lane quadrant this warp may access
     const int row_in_tile = quad * 32 + lane;  // TMEM lane == tile row
     const uint32_t trow = tbase + (static_cast<uint32_t>(quad * 32) << 16);
-    const unsigned long long p = P.p;
-#pragma unroll 1
-    for (int b = 0; b < NB_; ++b)
-#pragma unroll
-      for (int c0 = 0; c0 < NT; c0 += 32) tmem_st32_zero(trow + b * NT + c0);
+    tmem_zero_all<NB_, NT>(trow);
     tmem_wait_st();
     fence_before();
     __syncwarp();
     if (lane == 0) dev::mbar_arrive(tmem_empty);
+    constexpr int FULL = NT - NT % 32;
     int e = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       const Item it = item_of(t, P);
@@ -392,48 +487,11 @@ __global__ void __launch_bounds__(kThreads, 1) mwi8_kernel(const __grid_constant
         dev::mbar_wait(tmem_full, e & 1);
         fence_after();
 #pragma unroll 1
-        for (int c0 = 0; c0 < NT; c0 += 32) {
-          unsigned long long acc[32];
-#pragma unroll
-          for (int c = 0; c < 32; ++c) acc[c] = 0;
-#pragma unroll 1
-          for (int b = 0; b < NB_; ++b) {
-            uint32_t v[32];
-            tmem_ld32(trow + b * NT + c0, v);
-            tmem_wait_ld();
-            tmem_st32_zero(trow + b * NT + c0);
-            const unsigned long long g = P.gam[b], gs = P.gam_sh[b];
-#pragma unroll
-            for (int c = 0; c < 32; ++c) {
-              const unsigned long long s2 = acc[c] + shoup32(v[c], g, gs, p);
-              acc[c] = s2 >= p ? s2 - p : s2;
-            }
-          }
-          if (c0 + 32 >= NT) {  // every block consumed and re-zeroed: release TMEM
-            tmem_wait_st();
-            fence_before();
-            __syncwarp();
-            if (lane == 0) dev::mbar_arrive(tmem_empty);
-          }
-          if (row < P.m) {
-            double* dst = dst_row + c0;
-            const i64 col0 = col_base + c0;
-            if (seg > 0) {  // earlier segments' residues were parked in C by this thread
-              for (int c = 0; c < 32 && col0 + c < P.n; ++c) {
-                const unsigned long long s2 = acc[c] + static_cast<unsigned long long>(dst[c]);
-                acc[c] = s2 >= p ? s2 - p : s2;
-              }
-            }
-            if (col0 + 32 <= P.n && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-#pragma unroll
-              for (int c = 0; c < 32; c += 2)
-                *reinterpret_cast<double2*>(dst + c) =
-                    make_double2(static_cast<double>(acc[c]), static_cast<double>(acc[c + 1]));
-            } else {
-              for (int c = 0; c < 32 && col0 + c < P.n; ++c) dst[c] = static_cast<double>(acc[c]);
-            }
-          }
-        }
+        for (int c0 = 0; c0 < FULL; c0 += 32)
+          epi_chunk<32, NB_, NT>(P, trow, c0, NT % 32 == 0 && c0 + 32 >= NT, tmem_empty, lane, seg, row, col_base,
+                                 dst_row);
+        if constexpr (NT % 32 != 0)
+          epi_chunk<NT % 32, NB_, NT>(P, trow, FULL, true, tmem_empty, lane, seg, row, col_base, dst_row);
       }
     }
   }
