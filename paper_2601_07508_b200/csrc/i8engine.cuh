@@ -40,7 +40,7 @@ constexpr int kThreads = 192;      // 6 warps
 // per-tile epilogue over more work.
 template <int D>
 struct Cfg {
-  static constexpr int kNT = D == 1 ? 256 : D == 2 ? 128 : D <= 4 ? 64 : D == 5 ? 48 : D == 6 ? 40 : 32;
+  static constexpr int kNT = D == 1 ? 256 : D == 2 ? 128 : D == 3 ? 80 : D == 4 ? 64 : D == 5 ? 48 : D == 6 ? 40 : 32;
   static constexpr int kAStage = D * kBM * kBK;        // bytes: D digit tiles of 128 x 64
   static constexpr int kBStage = D * kNT * kBK;        // bytes: B_cat tile of (NT D) x 64
   static constexpr int kStageBytes = kAStage + kBStage;
