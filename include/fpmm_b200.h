@@ -49,9 +49,12 @@ typedef enum {
 /* engine selection (same results, different tensor-core path):
  *   DMMA: the paper's FP64 multiword product on the FP64 tensor pipe (mma.sync .f64)
  *   I8  : base-256 multiword words on tcgen05.mma.kind::i8 (int32 TMEM accumulators)
- * neither flag = the library default (I8) */
+ *   RNS : byte residues modulo pairwise-coprime m_i <= 256, one kind::i8 GEMM per
+ *         modulus, CRT reconstruction mod p fused into the epilogue
+ * no flag = the library default (I8) */
 #define FPMM_B200_ENGINE_DMMA 0x10u
 #define FPMM_B200_ENGINE_I8 0x20u
+#define FPMM_B200_ENGINE_RNS 0x40u
 
 /* product variants (multiword.hpp:113-254); all map to the same fused kernel */
 typedef enum {
@@ -112,6 +115,14 @@ int fpmm_b200_finish_plan(fpmm_b200_plan* plan, int64_t m, int64_t k, int64_t n)
 /* the fused kernel's internal K-block (terms between in-register reductions)
  * for balanced signed words; >= 4 for every (u,v,p) the reference admits */
 int fpmm_b200_kernel_block(uint64_t p, int u, int v, int64_t* lambda_k);
+/* RNS engine words: the smallest count n of the fixed pairwise-coprime byte
+ * moduli (256, 255, 253, 251, ...) whose product M covers the centred exact
+ * sum, 1000 M >= 2002 K floor(p/2)^2, and the CRT constants the fused
+ * epilogue uses: y_i = (M/m_i)^-1 mod m_i, g_i = round(2^24 y_i / m_i),
+ * W_i = y_i (M/m_i) mod p, Mp = M mod p.  Arrays hold FPMM_B200_RNS_MAX_MODULI. */
+#define FPMM_B200_RNS_MAX_MODULI 20
+int fpmm_b200_rns_plan(uint64_t p, int64_t k, int* nmod, uint32_t* moduli, uint32_t* y, uint32_t* g,
+                       uint64_t* W, uint64_t* Mp);
 
 /* mat.hpp:92-120 random_mat + driver.cpp:14-20 matrix_seed (synthetic inputs) */
 uint64_t fpmm_b200_mix_seed(uint64_t a, uint64_t b);

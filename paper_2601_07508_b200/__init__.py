@@ -25,7 +25,7 @@ __all__ = [
     "FpContext", "WordDecomposition", "ProductPlan", "Variant", "kVariants", "Timing",
     "is_prime_u64", "prev_prime", "bitsize", "word_base", "word_bound", "max_block_size",
     "mw_block_size", "variant_bit_limit", "variant_admits_bits", "select_variant",
-    "plan_for_modulus", "finish_plan", "kernel_block", "mix_seed", "matrix_seed", "random_mat",
+    "plan_for_modulus", "finish_plan", "kernel_block", "rns_plan", "mix_seed", "matrix_seed", "random_mat",
     "decompose", "mw_product", "mw_product_words", "mw_product_workspace",
     "mw_product_workspace_words", "mw_product_concat", "mw_product_concat_words",
     "block_gemm_mod", "GemmKernel", "kernel_by_name", "b200_kernel", "mw_product_device",
@@ -71,17 +71,18 @@ INPLACE_INVERSES = 0x4
 BCAST_RAW_B = 0x8
 ENGINE_DMMA = 0x10  # FP64 multiword on the FP64 tensor pipe (DMMA)
 ENGINE_I8 = 0x20    # base-256 multiword on tcgen05.mma.kind::i8 (TMEM int32 accumulators)
+ENGINE_RNS = 0x40   # byte residues mod coprime m_i <= 256, one kind::i8 GEMM per modulus, fused CRT
 ASYNC = 0x100
 PLAIN, WORKSPACE, CONCAT = 0, 1, 2
-_ENGINE_MASK = ENGINE_DMMA | ENGINE_I8
+_ENGINE_MASK = ENGINE_DMMA | ENGINE_I8 | ENGINE_RNS
 _default_engine_flags = 0
 
 
 def set_default_engine(name: Optional[str]) -> None:
-    """Engine used when a call passes no ENGINE_* flag: "i8", "dmma" or None
-    (the library default, the int8 tcgen05 engine)."""
+    """Engine used when a call passes no ENGINE_* flag: "i8", "rns", "dmma" or
+    None (the library default)."""
     global _default_engine_flags
-    _default_engine_flags = {"i8": ENGINE_I8, "dmma": ENGINE_DMMA, None: 0}[name]
+    _default_engine_flags = {"i8": ENGINE_I8, "rns": ENGINE_RNS, "dmma": ENGINE_DMMA, None: 0}[name]
 
 
 def _eng(flags: int) -> int:
@@ -136,6 +137,7 @@ def lib():
         "fpmm_b200_plan_for_modulus": (i32, [u64, i64, i64, i64, i32, u64, i64, C.POINTER(_Plan)]),
         "fpmm_b200_finish_plan": (i32, [C.POINTER(_Plan), i64, i64, i64]),
         "fpmm_b200_kernel_block": (i32, [u64, i32, i32, _i64p]),
+        "fpmm_b200_rns_plan": (i32, [u64, i64, C.POINTER(i32), vp, vp, vp, vp, _u64p]),
         "fpmm_b200_mix_seed": (u64, [u64, u64]),
         "fpmm_b200_matrix_seed": (u64, [u64, i32, i64, i64, i64, u64]),
         "fpmm_b200_random_mat": (i32, [i64, i64, u64, u64, _dp]),
@@ -352,6 +354,24 @@ def kernel_block(p: int, u: int, v: int) -> int:
     out = C.c_int64()
     _check(lib().fpmm_b200_kernel_block(p, u, v, C.byref(out)))
     return out.value
+
+
+RNS_MAX_MODULI = 20
+
+
+def rns_plan(p: int, k: int) -> dict:
+    """RNS engine words for residues < p and contraction length k: the byte
+    moduli and the CRT constants of the fused epilogue (fpmm_b200_rns_plan)."""
+    n = C.c_int()
+    mods = (C.c_uint32 * RNS_MAX_MODULI)()
+    y = (C.c_uint32 * RNS_MAX_MODULI)()
+    g = (C.c_uint32 * RNS_MAX_MODULI)()
+    W = (C.c_uint64 * RNS_MAX_MODULI)()
+    Mp = C.c_uint64()
+    _check(lib().fpmm_b200_rns_plan(p, k, C.byref(n), mods, y, g, W, C.byref(Mp)))
+    c = n.value
+    return {"n": c, "moduli": list(mods[:c]), "y": list(y[:c]), "g": list(g[:c]), "W": list(W[:c]),
+            "Mp": Mp.value}
 
 
 # ------------------------------------------------------------ synthetic inputs

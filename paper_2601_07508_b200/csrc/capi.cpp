@@ -119,6 +119,22 @@ int fpmm_b200_kernel_block(uint64_t p, int u, int v, int64_t* lambda_k) {
   });
 }
 
+int fpmm_b200_rns_plan(uint64_t p, int64_t k, int* nmod, uint32_t* moduli, uint32_t* y, uint32_t* g,
+                       uint64_t* W, uint64_t* Mp) {
+  return guarded([&] {
+    if (k < 0) throw Failure(FPMM_B200_EERROR, "k must be nonnegative");
+    const RnsPlan pl = rns_plan(p, k);
+    *nmod = pl.n;
+    for (int i = 0; i < pl.n; ++i) {
+      if (moduli) moduli[i] = pl.mod[i];
+      if (y) y[i] = pl.y[i];
+      if (g) g[i] = pl.g[i];
+      if (W) W[i] = pl.W[i];
+    }
+    if (Mp) *Mp = pl.Mp;
+  });
+}
+
 // mat.hpp:104-110 (splitmix64 step)
 uint64_t fpmm_b200_mix_seed(uint64_t a, uint64_t b) {
   uint64_t z = a + 0x9e3779b97f4a7c15ull * (b + 1);

@@ -14,6 +14,7 @@
 
 #include "i8engine.cuh"
 #include "kernels.cuh"
+#include "rnsengine.cuh"
 
 namespace fpmm_b200 {
 
@@ -150,7 +151,7 @@ int grid_for(i64 items, int threads) {
 }
 
 // Everything the kernels need for one (m, k, n, p, u, v) problem.
-enum Engine { kDmma = 0, kI8 = 1 };
+enum Engine { kDmma = 0, kI8 = 1, kRns = 2 };
 
 struct Job {
   i64 m, k, n;
@@ -164,6 +165,9 @@ struct Job {
   GemmParams gp{};
   DigitParams da{}, db{};
   i8::Params ip{};
+  int nmod = 0;  // RNS engine: moduli count
+  rns::Params rp{};
+  rns::PackParams rpp{};
 };
 
 template <typename F>
@@ -181,6 +185,7 @@ void dispatch_d(int D, F&& f) {
 }
 
 int resolve_engine(unsigned flags) {
+  if (flags & FPMM_B200_ENGINE_RNS) return kRns;
   if (flags & FPMM_B200_ENGINE_I8) return kI8;
   if (flags & FPMM_B200_ENGINE_DMMA) return kDmma;
   return kI8;  // library default: the int8 tcgen05 engine (same results, ~5-13x faster)
@@ -220,7 +225,59 @@ Job make_i8_job(i64 m, i64 k, i64 n, u64 p) {
   return j;
 }
 
+Job make_rns_job(i64 m, i64 k, i64 n, u64 p) {
+  Job j;
+  j.m = m, j.k = k, j.n = n, j.p = p, j.engine = kRns;
+  const RnsPlan pl = rns_plan(p, k);
+  j.nmod = pl.n;
+  j.BM = rns::kBM;
+  j.BN = rns::kNT;
+  j.MB = static_cast<int>((m + rns::kBM - 1) / rns::kBM);
+  j.NB = static_cast<int>((n + rns::kNT - 1) / rns::kNT);
+  j.KB = static_cast<int>((k + rns::kBK - 1) / rns::kBK);
+  j.per_rb_bytes = static_cast<size_t>(j.nmod) * j.KB * rns::kAStage;
+  j.apack_bytes = static_cast<size_t>(j.MB) * j.per_rb_bytes;
+  j.bpack_bytes = static_cast<size_t>(j.NB) * j.nmod * j.KB * rns::kBStage;
+  // a residue GEMM block read as u32 is exact while K_seg 255^2 < 2^32
+  const i64 seg_kb = std::max<i64>(1, static_cast<i64>(0xFFFFFFFFull / (255ull * 255ull)) / rns::kBK);
+  j.lambda_k = seg_kb * rns::kBK;
+  rns::Params& q = j.rp;
+  q.m = m, q.n = n, q.MB = j.MB, q.NB = j.NB, q.KB = j.KB;
+  q.nmod = j.nmod;
+  q.seg_kb = static_cast<int>(std::min<i64>(seg_kb, j.KB > 0 ? j.KB : 1));
+  q.kb_per_split = j.KB;
+  q.splits = 1;
+  q.split_stride = 0;
+  q.p = p;
+  q.mu = static_cast<unsigned long long>((static_cast<u128>(1) << 64) / p);
+  q.two32 = (u64{1} << 32) % p;
+  q.two32_sh = shoup(q.two32, p);
+  q.Mp = pl.Mp;
+  q.Mp_sh = shoup(pl.Mp, p);
+  rns::PackParams& pp = j.rpp;
+  pp.half_p = p / 2;
+  pp.nmod = j.nmod;
+  for (int i = 0; i < j.nmod; ++i) {
+    const u64 mi = pl.mod[i];
+    q.mod[i] = pp.mod[i] = static_cast<uint32_t>(mi);
+    q.c16[i] = static_cast<uint32_t>((u64{1} << 16) % mi);
+    q.magic[i] = pp.magic[i] = static_cast<uint32_t>(((u64{1} << 37) + mi - 1) / mi);
+    q.g[i] = pl.g[i];
+    q.w_lo[i] = static_cast<uint32_t>(pl.W[i]);
+    q.w_hi[i] = static_cast<uint32_t>(pl.W[i] >> 32);
+    pp.c1[i] = static_cast<uint32_t>((u64{1} << 18) % mi);
+    pp.c2[i] = static_cast<uint32_t>((u64{1} << 36) % mi);
+    pp.negadd[i] = static_cast<uint32_t>((mi - p % mi) % mi);
+  }
+  return j;
+}
+
 Job make_job(i64 m, i64 k, i64 n, u64 p, int u, int v, int engine = kDmma) {
+  if (engine == kRns) {
+    Job j = make_rns_job(m, k, n, p);
+    j.u = u, j.v = v;
+    return j;
+  }
   if (engine == kI8) {
     Job j = make_i8_job(m, k, n, p);
     j.u = u, j.v = v;
@@ -265,6 +322,16 @@ Job make_job(i64 m, i64 k, i64 n, u64 p, int u, int v, int engine = kDmma) {
 
 void launch_pack_a(const Job& j, const double* A, i64 lda, i64 rows, void* apack, int* err,
                    cudaStream_t s) {
+  if (j.engine == kRns) {
+    if (err && rows > 0 && j.k > 0)
+      check_residues_kernel<<<grid_for(rows * j.k, 256), 256, 0, s>>>(A, lda, rows, j.k, j.p, err);
+    const i64 mpad = ((rows + rns::kBM - 1) / rns::kBM) * rns::kBM;
+    const i64 items = mpad * j.KB * (rns::kBK / 16);
+    rns::pack_a_rns<<<grid_for(items, 256), 256, 0, s>>>(A, lda, rows, j.k, j.KB, mpad, j.rpp,
+                                                          static_cast<uint8_t*>(apack));
+    CUDA_OK(cudaGetLastError());
+    return;
+  }
   if (j.engine == kI8) {
     if (err && rows > 0 && j.k > 0)
       check_residues_kernel<<<grid_for(rows * j.k, 256), 256, 0, s>>>(A, lda, rows, j.k, j.p, err);
@@ -289,6 +356,15 @@ void launch_pack_a(const Job& j, const double* A, i64 lda, i64 rows, void* apack
 }
 
 void launch_pack_b(const Job& j, const double* B, i64 ldb, void* bpack, int* err, cudaStream_t s) {
+  if (j.engine == kRns) {
+    if (err && j.k > 0 && j.n > 0)
+      check_residues_kernel<<<grid_for(j.k * j.n, 256), 256, 0, s>>>(B, ldb, j.k, j.n, j.p, err);
+    const i64 tiles = static_cast<i64>(j.KB) * j.NB * (rns::kNT / 32);
+    rns::pack_b_rns<<<static_cast<unsigned>(std::min<i64>(std::max<i64>(tiles, 1), 148 * 32)), 128, 0, s>>>(
+        B, ldb, j.k, j.n, j.KB, j.NB, j.rpp, static_cast<uint8_t*>(bpack));
+    CUDA_OK(cudaGetLastError());
+    return;
+  }
   if (j.engine == kI8) {
     if (err && j.k > 0 && j.n > 0)
       check_residues_kernel<<<grid_for(j.k * j.n, 256), 256, 0, s>>>(B, ldb, j.k, j.n, j.p, err);
@@ -372,8 +448,62 @@ void launch_gemm_i8(const Job& j, const void* apack, const void* bpack, double* 
   }
 }
 
+void launch_gemm_rns(const Job& j, const void* apack, const void* bpack, double* C, i64 ldc, i64 rows,
+                     cudaStream_t s) {
+  rns::Params q = j.rp;
+  q.apack = static_cast<const uint8_t*>(apack);
+  q.bpack = static_cast<const uint8_t*>(bpack);
+  q.C = C;
+  q.ldc = ldc;
+  q.m = rows;
+  q.MB = static_cast<int>((rows + rns::kBM - 1) / rns::kBM);
+  // split-K when the output has too few tiles for the SMs (each slice runs
+  // its own CRT; partial residues are combined mod p), and one slice per
+  // exact int32 segment for long K (split-major: each wave streams one
+  // K-chunk of its panels)
+  const i64 tiles0 = static_cast<i64>(q.MB) * q.NB;
+  int splits = 1;
+  if (tiles0 > 0 && tiles0 < 148) {
+    const i64 want = (148 + tiles0 - 1) / tiles0;
+    splits = static_cast<int>(std::max<i64>(1, std::min<i64>({want, j.KB / 16, 32})));
+  }
+  if (j.KB > q.seg_kb) splits = std::max<int>(splits, (j.KB + q.seg_kb - 1) / q.seg_kb);
+  q.kb_per_split = (j.KB + splits - 1) / splits;
+  splits = (j.KB + q.kb_per_split - 1) / q.kb_per_split;
+  q.splits = splits;
+  int dev = 0;
+  CUDA_OK(cudaGetDevice(&dev));
+  DeviceCtx& dc = ctx(dev);
+  double* work = nullptr;
+  if (splits > 1) {
+    work = static_cast<double*>(dc.splitws.get(sizeof(double) * splits * rows * j.n));
+    q.C = work;
+    q.ldc = j.n;
+    q.split_stride = rows * j.n;
+  }
+  int sms = 148;
+  CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const i64 items = static_cast<i64>(q.MB) * q.NB * splits;
+  if (items > 0x7fffffff) throw Failure(FPMM_B200_EERROR, "problem too large for one launch");
+  const unsigned grid = static_cast<unsigned>(std::max<i64>(1, std::min<i64>(items, sms)));
+  q.scratch = static_cast<uint8_t*>(dc.scratch.get(static_cast<size_t>(grid) * j.nmod * rns::kSlotPerMod));
+  static bool configured[64] = {};
+  if (!configured[dev & 63]) {
+    CUDA_OK(cudaFuncSetAttribute(rns::rns_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, rns::kSmem));
+    configured[dev & 63] = true;
+  }
+  rns::rns_kernel<<<grid, rns::kThreads, rns::kSmem, s>>>(q);
+  CUDA_OK(cudaGetLastError());
+  if (splits > 1) {
+    i8::splitk_reduce_kernel<<<grid_for(rows * j.n, 256), 256, 0, s>>>(work, rows * j.n, splits, C, ldc, rows,
+                                                                        j.n, j.p);
+    CUDA_OK(cudaGetLastError());
+  }
+}
+
 void launch_gemm(const Job& j, const void* apack_v, const void* bpack_v, double* C, i64 ldc, i64 rows,
                  cudaStream_t s) {
+  if (j.engine == kRns) return launch_gemm_rns(j, apack_v, bpack_v, C, ldc, rows, s);
   if (j.engine == kI8) return launch_gemm_i8(j, apack_v, bpack_v, C, ldc, rows, s);
   const double* apack = static_cast<const double*>(apack_v);
   const double* bpack = static_cast<const double*>(bpack_v);
@@ -534,8 +664,10 @@ void product_prepared_device(const Prepared* h, const double* dB, i64 ldb, doubl
                              void* stream, unsigned flags, fpmm_b200_timing* tm) {
   std::lock_guard<std::recursive_mutex> lk(g_mu);
   if (!h) throw Failure(FPMM_B200_EERROR, "null prepared operand");
-  const unsigned fl = (flags & ~(FPMM_B200_ENGINE_DMMA | FPMM_B200_ENGINE_I8)) |
-                      (h->engine == kI8 ? FPMM_B200_ENGINE_I8 : FPMM_B200_ENGINE_DMMA) |
+  const unsigned fl = (flags & ~(FPMM_B200_ENGINE_DMMA | FPMM_B200_ENGINE_I8 | FPMM_B200_ENGINE_RNS)) |
+                      (h->engine == kRns  ? FPMM_B200_ENGINE_RNS
+                       : h->engine == kI8 ? FPMM_B200_ENGINE_I8
+                                          : FPMM_B200_ENGINE_DMMA) |
                       (h->flags & FPMM_B200_ALLOW_COMPOSITE);
   validate_product(h->p, h->u, h->v, lambda, h->m, h->k, n, fl);
   DeviceCtx& c = ctx(h->device);

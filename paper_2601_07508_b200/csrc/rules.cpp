@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <limits>
+#include <vector>
 
 #include "fpmm_b200.h"
 
@@ -239,5 +240,89 @@ i64 kernel_block(u64 p, int u, int v, int step) {
 }
 
 u64 shoup(u64 w, u64 p) { return static_cast<u64>((static_cast<u128>(w) << 64) / p); }
+
+}  // namespace fpmm_b200
+
+namespace fpmm_b200 {
+
+namespace {
+constexpr std::uint32_t kRnsModuli[kRnsMaxMod] = {256, 255, 253, 251, 247, 241, 239, 233, 229, 227,
+                                                  223, 217, 211, 199, 197, 193, 191, 181, 179, 173};
+
+// little-endian base-2^32 magnitudes
+using Big = std::vector<std::uint32_t>;
+void big_mul(Big& a, u64 f) {
+  u128 carry = 0;
+  for (auto& x : a) {
+    const u128 t = static_cast<u128>(x) * f + carry;
+    x = static_cast<std::uint32_t>(t);
+    carry = t >> 32;
+  }
+  for (; carry; carry >>= 32) a.push_back(static_cast<std::uint32_t>(carry));
+}
+bool big_ge(const Big& a, const Big& b) {
+  size_t na = a.size(), nb = b.size();
+  while (na > 1 && a[na - 1] == 0) --na;
+  while (nb > 1 && b[nb - 1] == 0) --nb;
+  if (na != nb) return na > nb;
+  for (size_t i = na; i-- > 0;)
+    if (a[i] != b[i]) return a[i] > b[i];
+  return true;
+}
+}  // namespace
+
+const std::uint32_t* rns_moduli_list() { return kRnsModuli; }
+
+RnsPlan rns_plan(u64 p, i64 k) {
+  if (p < 2) throw Failure(FPMM_B200_EERROR, "rns_plan: p must exceed 1");
+  const u64 h = p / 2, kk = static_cast<u64>(std::max<i64>(k, 1));
+  Big need{1};  // 2002 K h^2
+  big_mul(need, 2002);
+  big_mul(need, kk);
+  big_mul(need, h);
+  big_mul(need, h);
+  Big M{1000};
+  RnsPlan pl;
+  for (int n = 1; n <= kRnsMaxMod; ++n) {
+    big_mul(M, kRnsModuli[n - 1]);
+    if (big_ge(M, need)) {
+      pl.n = n;
+      break;
+    }
+  }
+  if (pl.n == 0)
+    throw Failure(FPMM_B200_EINFEASIBLE, "rns_plan: " + std::to_string(kRnsMaxMod) +
+                                             " byte moduli cannot cover K = " + std::to_string(k) + " at p = " +
+                                             std::to_string(p));
+  const int n = pl.n;
+  pl.Mp = 1 % p;
+  pl.log2M = 0;
+  for (int i = 0; i < n; ++i) {
+    pl.mod[i] = kRnsModuli[i];
+    pl.Mp = mulmod(pl.Mp, kRnsModuli[i] % p, p);
+    pl.log2M += std::log2(static_cast<double>(kRnsModuli[i]));
+  }
+  pl.log2X = 1.0 + std::log2(static_cast<double>(kk)) + 2.0 * std::log2(static_cast<double>(std::max<u64>(h, 1)));
+  for (int i = 0; i < n; ++i) {
+    const std::uint32_t mi = pl.mod[i];
+    u64 Mi_mod_mi = 1, Mi_mod_p = 1 % p;
+    for (int j = 0; j < n; ++j) {
+      if (j == i) continue;
+      Mi_mod_mi = Mi_mod_mi * (pl.mod[j] % mi) % mi;
+      Mi_mod_p = mulmod(Mi_mod_p, pl.mod[j] % p, p);
+    }
+    std::uint32_t y = 0;
+    for (std::uint32_t c = 1; c < mi; ++c)
+      if (Mi_mod_mi * c % mi == 1) {
+        y = c;
+        break;
+      }
+    if (y == 0 && mi > 1) throw Failure(FPMM_B200_EERROR, "rns_plan: moduli are not pairwise coprime");
+    pl.y[i] = y;
+    pl.g[i] = static_cast<std::uint32_t>(((static_cast<u64>(y) << 24) + mi / 2) / mi);
+    pl.W[i] = mulmod(y % p, Mi_mod_p, p);
+  }
+  return pl;
+}
 
 }  // namespace fpmm_b200

@@ -1,0 +1,132 @@
+"""GPU parity of the RNS tcgen05 engine (FPMM_B200_ENGINE_RNS).
+
+Same contract as the other engines: C is the unique residue matrix, so every
+comparison is bit-exact against the reference's outputs / the u128 oracle.
+The range tests drive X = sum a'b' to +-K floor(p/2)^2, where the CRT's
+rounding margin is thinnest.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2601_07508_b200 as F
+
+pytestmark = pytest.mark.gpu
+RNS = F.ENGINE_RNS
+
+
+def test_rns_small_exact():
+    p = F.prev_prime(1 << 20)
+    rng = np.random.default_rng(0)
+    A = rng.integers(0, p, size=(128, 64)).astype(np.float64)
+    B = rng.integers(0, p, size=(64, 256)).astype(np.float64)
+    C = F.mw_product(A, B, 1, 1, 64, F.FpContext.make(p), flags=RNS)
+    assert (C == O.exact_mod_gemm(A, B, p)).all()
+
+
+def test_rns_golden_vectors(golden):
+    for c in golden["cases"]:
+        p, A, B = O.seeded_inputs(c["m"], c["k"], c["n"], c["bits"], c["seed"])
+        C = F.mw_product(A, B, c["u"], c["v"], c["lam"], F.FpContext.make(p), flags=RNS)
+        assert O.fnv1a64(C) == c["fnv1a64"], c
+        if "C" in c:
+            assert [int(x) for x in C.ravel()] == c["C"]
+
+
+@pytest.mark.parametrize("bits", [3, 5, 8, 9, 16, 17, 20, 24, 25, 32, 33, 40, 41, 48, 49, 51, 52])
+def test_rns_every_modulus_count(bits):
+    p = F.prev_prime(1 << bits)
+    if p < 5:
+        pytest.skip("p < 5")
+    pl = F.plan_for_modulus(p, 100, 100, 100)
+    rng = np.random.default_rng(bits)
+    for (m, k, n) in ((1, 1, 1), (17, 33, 9), (129, 65, 257), (300, 517, 70), (256, 1000, 512)):
+        A = rng.integers(0, p, size=(m, k)).astype(np.float64)
+        B = rng.integers(0, p, size=(k, n)).astype(np.float64)
+        lam = min(pl.lambda_, k)
+        C = F.mw_product(A, B, pl.u, pl.v, lam, F.FpContext.make(p), flags=RNS)
+        assert (C == O.exact_mod_gemm(A, B, p)).all(), (bits, m, k, n)
+
+
+@pytest.mark.parametrize("bits", [8, 20, 33, 48, 52])
+@pytest.mark.parametrize("sign", [1, -1])
+def test_rns_crt_range_extremes(bits, sign):
+    """a' = b' = floor(p/2) (X = +K h^2) and a' = -b' (X = -K h^2)."""
+    p = F.prev_prime(1 << bits)
+    h = p // 2
+    m, k, n = 130, 3000, 300
+    A = np.full((m, k), float(h))
+    B = np.full((k, n), float(h if sign > 0 else h + 1))  # h + 1 centres to -h
+    pl = F.plan_for_modulus(p, m, k, n)
+    C = F.mw_product(A, B, pl.u, pl.v, min(pl.lambda_, k), F.FpContext.make(p), flags=RNS)
+    want = (sign * k * h * h) % p
+    assert (C == want).all()
+
+
+@pytest.mark.parametrize("bits", [20, 48, 52])
+def test_rns_long_k_segments(bits):
+    """K beyond one exact int32 segment (66048 terms): split-major slices, CRT per slice."""
+    p = F.prev_prime(1 << bits)
+    m, k, n = 130, 70000, 260
+    rng = np.random.default_rng(bits)
+    A = rng.integers(0, p, size=(m, k)).astype(np.float64)
+    B = rng.integers(0, p, size=(k, n)).astype(np.float64)
+    pl = F.plan_for_modulus(p, m, k, n)
+    C = F.mw_product(A, B, pl.u, pl.v, min(pl.lambda_, k), F.FpContext.make(p), flags=RNS)
+    assert (C == O.exact_mod_gemm(A, B, p)).all()
+
+
+def test_rns_worst_case_all_max():
+    p = F.prev_prime(1 << 52)
+    m, k, n = 200, 20000, 300
+    A = np.full((m, k), float(p - 1))
+    B = np.full((k, n), float(p - 1))
+    C = F.mw_product(A, B, 2, 2, 1, F.FpContext.make(p), flags=RNS)
+    assert (C == ((p - 1) * (p - 1) * k) % p).all()
+
+
+def test_rns_strided_device_and_split():
+    """Device tensors with leading dimensions, on an explicit stream; the
+    tall-skinny shape takes the split-K path."""
+    import torch
+    p = F.prev_prime(1 << 45)
+    rng = np.random.default_rng(3)
+    m, k, n = 300, 4096, 40
+    A = rng.integers(0, p, size=(m, k + 5)).astype(np.float64)
+    B = rng.integers(0, p, size=(k, n + 3)).astype(np.float64)
+    dA = torch.from_numpy(A).cuda()[:, :k]
+    dB = torch.from_numpy(B).cuda()[:, :n]
+    dC = torch.zeros((m, n + 7), dtype=torch.float64, device="cuda")[:, :n]
+    s = torch.cuda.Stream()
+    pl = F.plan_for_modulus(p, m, k, n)
+    F.mw_product_device(dA, dB, dC, p, pl.u, pl.v, pl.lambda_, stream=s, flags=RNS)
+    s.synchronize()
+    want = O.exact_mod_gemm(A[:, :k], B[:, :n], p)
+    assert (dC.cpu().numpy() == want).all()
+
+
+def test_rns_freivalds_4096():
+    import torch
+    p = F.prev_prime(1 << 52)
+    m = k = n = 4096
+    A = torch.empty((m, k), dtype=torch.float64, device="cuda")
+    B = torch.empty((k, n), dtype=torch.float64, device="cuda")
+    C = torch.empty((m, n), dtype=torch.float64, device="cuda")
+    F.random_residues_device(A, p, 11)
+    F.random_residues_device(B, p, 12)
+    F.mw_product_device(A, B, C, p, 2, 2, 1, flags=RNS)
+    An, Bn, Cn = A.cpu().numpy(), B.cpu().numpy(), C.cpu().numpy()
+    assert O.freivalds(An, Bn, Cn, p, trials=2) == 0
+    rows = np.random.default_rng(5).integers(0, m, size=8)
+    assert (Cn[rows] == O.exact_mod_gemm(An[rows], Bn, p)).all()
+
+
+def test_rns_matches_other_engines():
+    p = F.prev_prime(1 << 37)
+    rng = np.random.default_rng(9)
+    A = rng.integers(0, p, size=(333, 777)).astype(np.float64)
+    B = rng.integers(0, p, size=(777, 555)).astype(np.float64)
+    pl = F.plan_for_modulus(p, 333, 777, 555)
+    outs = [F.mw_product(A, B, pl.u, pl.v, pl.lambda_, F.FpContext.make(p), flags=e)
+            for e in (F.ENGINE_RNS, F.ENGINE_I8, F.ENGINE_DMMA)]
+    assert (outs[0] == outs[1]).all() and (outs[0] == outs[2]).all()

@@ -1,0 +1,148 @@
+"""Host rules of the RNS engine (rnsengine.cuh), checked on CPU.
+
+The engine represents centred residues by their residues modulo byte moduli
+and rebuilds X = sum_k a'_k b'_k mod p by the CRT in its epilogue.  These
+tests pin (1) the modulus count against the exact range bound with Python
+integers, (2) every CRT constant the library exports, (3) the device's
+fixed-point / Shoup / Barrett reconstruction, emulated here with the same
+u64 arithmetic, at the extreme values of X, and (4) the umulhi magic-number
+reduction used by the packers and the epilogue.
+"""
+import math
+import random
+
+import numpy as np
+import pytest
+
+import paper_2601_07508_b200 as F
+
+MASK64 = (1 << 64) - 1
+
+
+def prod(xs):
+    r = 1
+    for x in xs:
+        r *= x
+    return r
+
+
+@pytest.mark.parametrize("bits", [3, 8, 16, 20, 24, 25, 32, 33, 40, 41, 48, 49, 51, 52])
+@pytest.mark.parametrize("k", [1, 64, 8192, 66048, 262144])
+def test_modulus_count_is_minimal_and_covers_the_range(bits, k):
+    p = F.prev_prime(1 << bits)
+    pl = F.rns_plan(p, k)
+    mods = pl["moduli"]
+    h = p // 2
+    assert 1000 * prod(mods) >= 2002 * k * h * h
+    assert 1000 * prod(mods[:-1]) < 2002 * k * h * h or len(mods) == 1
+    for i in range(len(mods)):
+        for j in range(i):
+            assert math.gcd(mods[i], mods[j]) == 1
+
+
+def test_modulus_count_against_digit_products():
+    """The point of the engine: far fewer int8 GEMMs than the D^2 digit products."""
+    for bits, n_max in ((20, 7), (32, 10), (40, 12), (48, 14), (52, 15)):
+        p = F.prev_prime(1 << bits)
+        assert F.rns_plan(p, 8192)["n"] <= n_max
+        d = (bits + 7) // 8
+        assert F.rns_plan(p, 8192)["n"] < d * d or bits <= 24
+
+
+@pytest.mark.parametrize("bits", [5, 20, 33, 52])
+def test_crt_constants(bits):
+    p = F.prev_prime(1 << bits)
+    pl = F.rns_plan(p, 8192)
+    mods = pl["moduli"]
+    M = prod(mods)
+    assert pl["Mp"] == M % p
+    for i, m in enumerate(mods):
+        Mi = M // m
+        assert (pl["y"][i] * Mi) % m == 1
+        assert pl["g"][i] == ((pl["y"][i] << 24) + m // 2) // m
+        assert pl["W"][i] == (pl["y"][i] * Mi) % p
+
+
+def shoup(w, p):
+    return (w << 64) // p
+
+
+def shoup_mulmod(t, w, ws, p):
+    q = (t * ws) >> 64
+    r = (t * w - q * p) & MASK64
+    return r - p if r >= p else r
+
+
+def barrett(x, p):
+    mu = (1 << 64) // p
+    q = (x * mu) >> 64
+    r = (x - q * p) & MASK64
+    return r - p if r >= p else r
+
+
+def device_crt(X, p, pl):
+    """crt8() of rnsengine.cuh on the residues of X, in the kernel's u64 arithmetic."""
+    s_lo = s_hi = f = 0
+    for m, g, W in zip(pl["moduli"], pl["g"], pl["W"]):
+        r = X % m
+        s_lo += r * (W & 0xFFFFFFFF)
+        s_hi += r * (W >> 32)
+        f += r * g
+    assert s_lo < 1 << 64 and s_hi < 1 << 64 and f < 1 << 64
+    t = (f + (1 << 23)) >> 24
+    two32 = (1 << 32) % p
+    hi = shoup_mulmod(s_hi, two32, shoup(two32, p), p)
+    s = barrett(hi + s_lo, p)
+    tm = shoup_mulmod(t, pl["Mp"], shoup(pl["Mp"], p), p)
+    return s - tm if s >= tm else s + p - tm
+
+
+@pytest.mark.parametrize("bits", [3, 8, 20, 25, 33, 40, 48, 52])
+@pytest.mark.parametrize("k", [1, 100, 8192, 66048])
+def test_device_crt_reconstruction_at_the_range_extremes(bits, k):
+    p = F.prev_prime(1 << bits)
+    pl = F.rns_plan(p, k)
+    h = p // 2
+    xmax = k * h * h
+    rng = random.Random(bits * 1000 + k)
+    cases = [0, 1, -1, xmax, -xmax, xmax - 1, -xmax + 1, h * h, -h * h]
+    cases += [rng.randint(-xmax, xmax) for _ in range(300)]
+    for X in cases:
+        assert device_crt(X, p, pl) == X % p, X
+
+
+@pytest.mark.parametrize("m", [256, 255, 253, 251, 247, 241, 217, 173])
+def test_magic_reduction_exhaustive_epilogue_range(m):
+    """mod_small(s) = s - (umulhi(s, ceil(2^37/m)) >> 5) m for every s < 2^24
+    (the epilogue's range); sampled up to 2^27 (the packers')."""
+    magic = ((1 << 37) + m - 1) // m
+    assert magic < 1 << 32
+    s = np.arange(0, 1 << 24, dtype=np.uint64)
+    q = ((s * np.uint64(magic)) >> np.uint64(32)) >> np.uint64(5)
+    assert np.array_equal(s - q * np.uint64(m), s % np.uint64(m))
+    s = np.random.default_rng(m).integers(0, 1 << 27, size=1 << 20, dtype=np.uint64)
+    s = np.concatenate([s, np.arange((1 << 27) - 4096, 1 << 27, dtype=np.uint64)])
+    q = ((s * np.uint64(magic)) >> np.uint64(32)) >> np.uint64(5)
+    assert np.array_equal(s - q * np.uint64(m), s % np.uint64(m))
+
+
+def test_packer_residue_split():
+    """residues16(): x mod m from 18-bit limbs plus the centring offset."""
+    p = F.prev_prime(1 << 52)
+    pl = F.rns_plan(p, 8192)
+    rng = random.Random(7)
+    xs = [0, 1, p // 2, p // 2 + 1, p - 1] + [rng.randrange(p) for _ in range(2000)]
+    for m in pl["moduli"]:
+        c1, c2, na = (1 << 18) % m, (1 << 36) % m, (m - p % m) % m
+        for x in xs:
+            x0, x1, x2 = x & 0x3FFFF, (x >> 18) & 0x3FFFF, x >> 36
+            neg = 1 if x > p // 2 else 0
+            s = x0 + x1 * c1 + x2 * c2 + neg * na
+            assert s < 1 << 27
+            centred = x - p if neg else x
+            assert s % m == centred % m
+
+
+def test_infeasible_range_raises():
+    with pytest.raises(F.InfeasibleError):
+        F.rns_plan(F.prev_prime(1 << 52), 1 << 60)
