@@ -3,6 +3,7 @@
 #include "engine.hpp"
 
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include "nccl_loader.hpp"
 
 #include <algorithm>
@@ -230,14 +231,14 @@ Job make_rns_job(i64 m, i64 k, i64 n, u64 p) {
   j.m = m, j.k = k, j.n = n, j.p = p, j.engine = kRns;
   const RnsPlan pl = rns_plan(p, k);
   j.nmod = pl.n;
-  j.BM = rns::kBM;
+  j.BM = rns::kPairM;  // pair tiles: 256 x 256
   j.BN = rns::kNT;
-  j.MB = static_cast<int>((m + rns::kBM - 1) / rns::kBM);
-  j.NB = static_cast<int>((n + rns::kNT - 1) / rns::kNT);
+  j.MB = static_cast<int>((m + j.BM - 1) / j.BM);
+  j.NB = static_cast<int>((n + j.BN - 1) / j.BN);
   j.KB = static_cast<int>((k + rns::kBK - 1) / rns::kBK);
-  j.per_rb_bytes = static_cast<size_t>(j.nmod) * j.KB * rns::kAStage;
+  j.per_rb_bytes = static_cast<size_t>(2) * j.nmod * j.KB * rns::kAStage;  // per 256 rows
   j.apack_bytes = static_cast<size_t>(j.MB) * j.per_rb_bytes;
-  j.bpack_bytes = static_cast<size_t>(j.NB) * j.nmod * j.KB * rns::kBStage;
+  j.bpack_bytes = static_cast<size_t>(2) * j.NB * j.nmod * j.KB * rns::kBStage;
   // a residue GEMM block read as u32 is exact while K_seg 255^2 < 2^32
   const i64 seg_kb = std::max<i64>(1, static_cast<i64>(0xFFFFFFFFull / (255ull * 255ull)) / rns::kBK);
   j.lambda_k = seg_kb * rns::kBK;
@@ -255,7 +256,7 @@ Job make_rns_job(i64 m, i64 k, i64 n, u64 p) {
   q.Mp = pl.Mp;
   q.Mp_sh = shoup(pl.Mp, p);
   rns::PackParams& pp = j.rpp;
-  pp.half_p = p / 2;
+  pp.half_p = static_cast<double>(p / 2);
   pp.nmod = j.nmod;
   for (int i = 0; i < j.nmod; ++i) {
     const u64 mi = pl.mod[i];
@@ -265,9 +266,15 @@ Job make_rns_job(i64 m, i64 k, i64 n, u64 p) {
     q.g[i] = pl.g[i];
     q.w_lo[i] = static_cast<uint32_t>(pl.W[i]);
     q.w_hi[i] = static_cast<uint32_t>(pl.W[i] >> 32);
-    pp.c1[i] = static_cast<uint32_t>((u64{1} << 18) % mi);
-    pp.c2[i] = static_cast<uint32_t>((u64{1} << 36) % mi);
-    pp.negadd[i] = static_cast<uint32_t>((mi - p % mi) % mi);
+    // dp4a weights: byte j of wlo/whi = 256^j mod m (j = 0..6); whi byte 3
+    // weighs the centring flag with the residue offset of x - p
+    pp.wlo[i] = pp.whi[i] = 0;
+    for (int jj = 0; jj < 7; ++jj) {
+      const uint32_t w = static_cast<uint32_t>(powmod(256 % mi, jj, mi));
+      if (jj < 4) pp.wlo[i] |= w << (8 * jj);
+      else pp.whi[i] |= w << (8 * (jj - 4));
+    }
+    pp.whi[i] |= static_cast<uint32_t>((mi - p % mi) % mi) << 24;
   }
   return j;
 }
@@ -325,7 +332,7 @@ void launch_pack_a(const Job& j, const double* A, i64 lda, i64 rows, void* apack
   if (j.engine == kRns) {
     if (err && rows > 0 && j.k > 0)
       check_residues_kernel<<<grid_for(rows * j.k, 256), 256, 0, s>>>(A, lda, rows, j.k, j.p, err);
-    const i64 mpad = ((rows + rns::kBM - 1) / rns::kBM) * rns::kBM;
+    const i64 mpad = ((rows + rns::kPairM - 1) / rns::kPairM) * rns::kPairM;
     const i64 items = mpad * j.KB * (rns::kBK / 16);
     rns::pack_a_rns<<<grid_for(items, 256), 256, 0, s>>>(A, lda, rows, j.k, j.KB, mpad, j.rpp,
                                                           static_cast<uint8_t*>(apack));
@@ -359,9 +366,9 @@ void launch_pack_b(const Job& j, const double* B, i64 ldb, void* bpack, int* err
   if (j.engine == kRns) {
     if (err && j.k > 0 && j.n > 0)
       check_residues_kernel<<<grid_for(j.k * j.n, 256), 256, 0, s>>>(B, ldb, j.k, j.n, j.p, err);
-    const i64 tiles = static_cast<i64>(j.KB) * j.NB * (rns::kNT / 32);
+    const i64 tiles = static_cast<i64>(j.KB) * (2 * j.NB) * (rns::kBH / 32);
     rns::pack_b_rns<<<static_cast<unsigned>(std::min<i64>(std::max<i64>(tiles, 1), 148 * 32)), 128, 0, s>>>(
-        B, ldb, j.k, j.n, j.KB, j.NB, j.rpp, static_cast<uint8_t*>(bpack));
+        B, ldb, j.k, j.n, j.KB, 2 * j.NB, j.rpp, static_cast<uint8_t*>(bpack));
     CUDA_OK(cudaGetLastError());
     return;
   }
@@ -448,23 +455,50 @@ void launch_gemm_i8(const Job& j, const void* apack, const void* bpack, double* 
   }
 }
 
+// 2-D uint8 tensor map over `bytes` of a packed operand viewed as 128-byte
+// rows, box 128 x 64 (one 8 KB chunk); the encoder comes from the driver
+// through the runtime (no libcuda link dependency).
+CUtensorMap chunk_map(const void* base, size_t bytes) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q{};
+    void* fn = nullptr;
+    CUDA_OK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess)
+      throw Failure(FPMM_B200_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  CUtensorMap m{};
+  const cuuint64_t dims[2] = {128, std::max<cuuint64_t>(64, bytes / 128)};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {128, 64};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Failure(FPMM_B200_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return m;
+}
+
 void launch_gemm_rns(const Job& j, const void* apack, const void* bpack, double* C, i64 ldc, i64 rows,
                      cudaStream_t s) {
   rns::Params q = j.rp;
   q.apack = static_cast<const uint8_t*>(apack);
   q.bpack = static_cast<const uint8_t*>(bpack);
+  q.tmA = chunk_map(apack, static_cast<size_t>((rows + rns::kPairM - 1) / rns::kPairM) * j.per_rb_bytes);
+  q.tmB = chunk_map(bpack, j.bpack_bytes);
   q.C = C;
   q.ldc = ldc;
   q.m = rows;
-  q.MB = static_cast<int>((rows + rns::kBM - 1) / rns::kBM);
-  // split-K when the output has too few tiles for the SMs (each slice runs
+  q.MB = static_cast<int>((rows + rns::kPairM - 1) / rns::kPairM);
+  // split-K when the output has too few pair tiles for the SM pairs (each slice runs
   // its own CRT; partial residues are combined mod p), and one slice per
   // exact int32 segment for long K (split-major: each wave streams one
   // K-chunk of its panels)
   const i64 tiles0 = static_cast<i64>(q.MB) * q.NB;
   int splits = 1;
-  if (tiles0 > 0 && tiles0 < 148) {
-    const i64 want = (148 + tiles0 - 1) / tiles0;
+  if (tiles0 > 0 && tiles0 < 74) {
+    const i64 want = (74 + tiles0 - 1) / tiles0;
     splits = static_cast<int>(std::max<i64>(1, std::min<i64>({want, j.KB / 16, 32})));
   }
   if (j.KB > q.seg_kb) splits = std::max<int>(splits, (j.KB + q.seg_kb - 1) / q.seg_kb);
@@ -485,7 +519,8 @@ void launch_gemm_rns(const Job& j, const void* apack, const void* bpack, double*
   CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const i64 items = static_cast<i64>(q.MB) * q.NB * splits;
   if (items > 0x7fffffff) throw Failure(FPMM_B200_EERROR, "problem too large for one launch");
-  const unsigned grid = static_cast<unsigned>(std::max<i64>(1, std::min<i64>(items, sms)));
+  // persistent CTA pairs (clusters of 2 on neighbouring SMs)
+  const unsigned grid = 2 * static_cast<unsigned>(std::max<i64>(1, std::min<i64>(items, sms / 2)));
   q.scratch = static_cast<uint8_t*>(dc.scratch.get(static_cast<size_t>(grid) * j.nmod * rns::kSlotPerMod));
   static bool configured[64] = {};
   if (!configured[dev & 63]) {

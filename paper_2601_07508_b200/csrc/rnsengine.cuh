@@ -27,6 +27,8 @@
 // lane quadrant w % 4, column half (w - 2) / 4).
 #pragma once
 
+#include <cuda.h>
+
 #include <cstdint>
 
 #include "device_common.cuh"
@@ -38,28 +40,33 @@ namespace rns {
 using i64 = std::int64_t;
 
 constexpr int kMaxMod = 20;
-constexpr int kBM = 128;            // rows per tile (MMA M)
-constexpr int kNT = 256;            // columns per tile (MMA N)
-constexpr int kBK = 64;             // k bytes per pipeline stage
-constexpr int kKSteps = kBK / 32;   // MMA K = 32 for kind::i8
-constexpr int kAStage = kBM * kBK;  // 8 KB
-constexpr int kBStage = kNT * kBK;  // 16 KB
+constexpr int kBM = 128;             // rows per CTA (each CTA's half of the pair's M = 256)
+constexpr int kNT = 256;             // columns per tile (MMA N)
+constexpr int kBH = kNT / 2;         // B columns held by each CTA of the pair
+constexpr int kPairM = 2 * kBM;      // rows per pair tile
+constexpr int kBK = 64;              // k bytes per pipeline stage
+constexpr int kKSteps = kBK / 32;    // MMA K = 32 for kind::i8
+constexpr int kAStage = kBM * kBK;   // 8 KB: this CTA's 128 rows of A
+constexpr int kBStage = kBH * kBK;   // 8 KB: this CTA's 128 columns of B
 constexpr int kStageBytes = kAStage + kBStage;
-constexpr int kStages = 8;
-constexpr int kThreads = 320;       // 10 warps
+constexpr int kStages = 12;
+constexpr int kThreads = 320;        // 10 warps
 constexpr int kEpiWarps = 8;
 constexpr int kSmem = kStages * kStageBytes + 1024;
-constexpr int kSlotPerMod = kBM * kNT;  // scratch bytes per modulus per tile (32 KB)
-constexpr int kGroup = 12;              // tile-rows per rasterisation group
+constexpr int kSlotPerMod = kBM * kNT;  // scratch bytes per modulus per CTA tile (32 KB)
+constexpr int kGroup = 6;               // pair-tile rows per rasterisation group
 
 // Per-modulus constants (host: rns_plan in rules.cpp).
 struct Params {
-  const uint8_t* apack;  // [m-block][modulus][k-block] chunks of kAStage bytes
-  const uint8_t* bpack;  // [n-block][modulus][k-block] chunks of kBStage bytes
+  // 2-D byte views (128-byte rows) of the packed operands for the pair TMA
+  // loads; a chunk of 8 KB is one 128 x 64 box at row 64 * chunk
+  CUtensorMap tmA, tmB;
+  const uint8_t* apack;  // [128-row block][modulus][k-block] chunks of kAStage bytes
+  const uint8_t* bpack;  // [128-column block][modulus][k-block] chunks of kBStage bytes
   double* C;
   uint8_t* scratch;      // per CTA: nmod * kSlotPerMod bytes
   i64 ldc, m, n;
-  int MB, NB, KB;
+  int MB, NB, KB;    // pair tiles (256 x 256) along m and n; 64-byte k-blocks
   int nmod;
   int seg_kb;        // k-blocks per exact int32 segment
   int kb_per_split;  // split-K: k-blocks per slice
@@ -76,12 +83,11 @@ struct Params {
 };
 
 struct PackParams {
-  unsigned long long half_p;  // floor(p/2): x > half_p is centred to x - p
+  double half_p;  // floor(p/2): x > half_p is centred to x - p
   int nmod;
   uint32_t mod[kMaxMod];
-  uint32_t c1[kMaxMod];      // 2^18 mod m
-  uint32_t c2[kMaxMod];      // 2^36 mod m
-  uint32_t negadd[kMaxMod];  // (m - p mod m) mod m: residue offset of x - p
+  uint32_t wlo[kMaxMod];    // bytes (256^j mod m), j = 0..3
+  uint32_t whi[kMaxMod];    // bytes (256^j mod m), j = 4..6, and (m - p mod m) mod m in byte 3
   uint32_t magic[kMaxMod];
 };
 
@@ -89,30 +95,31 @@ __device__ __forceinline__ uint32_t mod_small(uint32_t s, uint32_t m, uint32_t m
   return s - (__umulhi(s, magic) >> 5) * m;
 }
 
+// x < 2^52 as two words of base-256 digits: lo = digits 0..3, hi = digits
+// 4..6 plus the centring flag [x > p/2] in byte 3.  The residue of the
+// centred value mod m is then dp4a(lo, wlo) + dp4a(hi, whi) (< 2^19) mod m.
+__device__ __forceinline__ void digits16(const double (&xs)[16], double half_p, uint32_t (&lo)[16],
+                                         uint32_t (&hi)[16]) {
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    // 2^52 + x has the integer x in its significand (x < 2^52)
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(xs[e] + 4503599627370496.0));
+    lo[e] = static_cast<uint32_t>(b);
+    hi[e] = (static_cast<uint32_t>(b >> 32) & 0xFFFFFu) | (xs[e] > half_p ? 0x1000000u : 0u);
+  }
+}
+
 // 16 residues (one 16-byte k row of a core matrix) of modulus i
-__device__ __forceinline__ uint4 residues16(const uint32_t (&x0)[16], const uint32_t (&x1)[16],
-                                            const uint32_t (&x2)[16], const uint32_t (&ng)[16],
-                                            const PackParams& P, int i) {
-  const uint32_t m = P.mod[i], c1 = P.c1[i], c2 = P.c2[i], na = P.negadd[i], mg = P.magic[i];
+__device__ __forceinline__ uint4 residues16(const uint32_t (&lo)[16], const uint32_t (&hi)[16], const PackParams& P,
+                                            int i) {
+  const uint32_t m = P.mod[i], wl = P.wlo[i], wh = P.whi[i], mg = P.magic[i];
   uint32_t w[4] = {0, 0, 0, 0};
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
-    const uint32_t s = x0[e] + x1[e] * c1 + x2[e] * c2 + ng[e] * na;  // < 2^27
+    const uint32_t s = __dp4a(lo[e], wl, __dp4a(hi[e], wh, 0u));
     w[e / 4] |= mod_small(s, m, mg) << (8 * (e % 4));
   }
   return make_uint4(w[0], w[1], w[2], w[3]);
-}
-
-__device__ __forceinline__ void split16(const double (&xs)[16], unsigned long long half_p, uint32_t (&x0)[16],
-                                        uint32_t (&x1)[16], uint32_t (&x2)[16], uint32_t (&ng)[16]) {
-#pragma unroll
-  for (int e = 0; e < 16; ++e) {
-    const unsigned long long x = static_cast<unsigned long long>(xs[e]);
-    x0[e] = static_cast<uint32_t>(x) & 0x3FFFFu;
-    x1[e] = static_cast<uint32_t>(x >> 18) & 0x3FFFFu;
-    x2[e] = static_cast<uint32_t>(x >> 36);
-    ng[e] = x > half_p ? 1u : 0u;
-  }
 }
 
 // A: m x k residues -> N residue planes in the canonical K-major core-matrix
@@ -151,33 +158,33 @@ __global__ void __launch_bounds__(256) pack_a_rns(const double* __restrict__ A, 
 #pragma unroll
       for (int e = 0; e < 16; ++e) xs[e] = 0.0;
     }
-    uint32_t x0[16], x1[16], x2[16], ng[16];
-    split16(xs, P.half_p, x0, x1, x2, ng);
+    uint32_t lo[16], hi[16];
+    digits16(xs, P.half_p, lo, hi);
     const i64 rb = row / kBM, kb = kc / (kBK / 16);
     const int c = static_cast<int>(kc % (kBK / 16)), g = static_cast<int>((row % kBM) / 8);
     uint8_t* base = out + ((rb * P.nmod) * KB + kb) * static_cast<i64>(kAStage) + ((c * (kBM / 8) + g) * 8 + r8) * 16;
 #pragma unroll 1
     for (int i = 0; i < P.nmod; ++i)
-      *reinterpret_cast<uint4*>(base + static_cast<i64>(i) * KB * kAStage) = residues16(x0, x1, x2, ng, P, i);
+      *reinterpret_cast<uint4*>(base + static_cast<i64>(i) * KB * kAStage) = residues16(lo, hi, P, i);
   }
 }
 
-// B: k x n residues -> N residue planes of 256-column blocks, K-major.
-// Chunk (cb, i, kb), kBStage bytes: [k16 c (4)][column group (32)][column (8)][16 B].
+// B: k x n residues -> N residue planes of 128-column blocks, K-major.
+// Chunk (cb, i, kb), kBStage bytes: [k16 c (4)][column group (16)][column (8)][16 B].
 // A 128-thread block transposes a 64 (k) x 32 (column) tile through shared memory.
 __global__ void __launch_bounds__(128) pack_b_rns(const double* __restrict__ B, i64 ldb, i64 k, i64 n, int KB,
-                                                  int NB, const __grid_constant__ PackParams P,
+                                                  int NB128, const __grid_constant__ PackParams P,
                                                   uint8_t* __restrict__ out) {
-  constexpr int SW = 32, SUB = kNT / SW;
+  constexpr int SW = 32, SUB = kBH / SW;
   __shared__ double tile[kBK][SW + 1];
-  const i64 tiles = static_cast<i64>(KB) * NB * SUB;
+  const i64 tiles = static_cast<i64>(KB) * NB128 * SUB;
   for (i64 t = blockIdx.x; t < tiles; t += gridDim.x) {
     const int sb = static_cast<int>(t % SUB);
-    const i64 cb = (t / SUB) % NB, kb = t / (SUB * static_cast<i64>(NB));
+    const i64 cb = (t / SUB) % NB128, kb = t / (SUB * static_cast<i64>(NB128));
     __syncthreads();
     for (int e = threadIdx.x; e < kBK * SW; e += blockDim.x) {
       const int kr = e / SW, cc = e % SW;
-      const i64 kk = kb * kBK + kr, col = cb * kNT + sb * SW + cc;
+      const i64 kk = kb * kBK + kr, col = cb * kBH + sb * SW + cc;
       tile[kr][cc] = (kk < k && col < n) ? B[kk * ldb + col] : 0.0;
     }
     __syncthreads();
@@ -185,17 +192,19 @@ __global__ void __launch_bounds__(128) pack_b_rns(const double* __restrict__ B, 
     double xs[16];
 #pragma unroll
     for (int e = 0; e < 16; ++e) xs[e] = tile[q * 16 + e][cc];
-    uint32_t x0[16], x1[16], x2[16], ng[16];
-    split16(xs, P.half_p, x0, x1, x2, ng);
+    uint32_t lo[16], hi[16];
+    digits16(xs, P.half_p, lo, hi);
     const int nn = sb * SW + cc, g = nn / 8, r8 = nn % 8;
-    uint8_t* base = out + ((cb * P.nmod) * KB + kb) * static_cast<i64>(kBStage) + ((q * (kNT / 8) + g) * 8 + r8) * 16;
+    uint8_t* base = out + ((cb * P.nmod) * KB + kb) * static_cast<i64>(kBStage) + ((q * (kBH / 8) + g) * 8 + r8) * 16;
 #pragma unroll 1
     for (int i = 0; i < P.nmod; ++i)
-      *reinterpret_cast<uint4*>(base + static_cast<i64>(i) * KB * kBStage) = residues16(x0, x1, x2, ng, P, i);
+      *reinterpret_cast<uint4*>(base + static_cast<i64>(i) * KB * kBStage) = residues16(lo, hi, P, i);
   }
 }
 
 // ------------------------------------------------------------------ GEMM
+// Work item t (0 <= t < MB * NB * splits) -> pair tile (tm, tn), split ks;
+// grouped rasterisation keeps a wave's panels of one modulus in L2.
 struct Item {
   int tm, tn, ks;
 };
@@ -295,17 +304,86 @@ __device__ __forceinline__ void crt8(const Params& P, uint8_t* slot, int half, i
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 1) rns_kernel(const __grid_constant__ Params P) {
+// ---- CTA-pair plumbing ----
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+// shared::cluster address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t peer_addr(const void* p, uint32_t rank) {
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(out) : "r"(dev::smem_u32(p)), "r"(rank));
+  return out;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra LAB_DONE;\n"
+      "bra LAB_WAIT;\n"
+      "LAB_DONE:\n"
+      "}\n" ::"r"(dev::smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mma_i8_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  const uint32_t z = 0;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(z));
+}
+// Pair TMA load of one 8 KB chunk (row `row` of the 128-byte view) into this
+// CTA's shared memory, completing on the LEADER's barrier at the same offset
+// (peer bit cleared), so the leader's one barrier tracks both halves.
+__device__ __forceinline__ void tma_pair_load(void* dst, const CUtensorMap* map, int row, uint64_t* bar) {
+  const uint32_t leader_bar = dev::smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];\n" ::"r"(dev::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(row), "r"(leader_bar)
+      : "memory");
+}
+// arrive on the barrier at this offset in both CTAs of the pair once the MMAs issued so far completed
+__device__ __forceinline__ void commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+          dev::smem_u32(bar)),
+      "h"(static_cast<uint16_t>(0x3))
+      : "memory");
+}
+
+// The pair (cluster of 2 CTAs on neighbouring SMs) computes a 256 x 256 tile:
+// CTA r holds rows 128 r.. of A and columns 128 r.. of B in its shared
+// memory and rows 128 r.. of the accumulator in its TMEM; the leader (r = 0)
+// issues M=256 N=256 K=32 cta_group::2 MMAs that read both halves.  Each SM
+// so streams 8 KB of A and 8 KB of B per 128-cycle k-step (64 B/clk).
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_kernel(const __grid_constant__ Params P) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;
   uint8_t* sB = smem + kStages * kAStage;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);  // leader: both halves landed
   uint64_t* empty = full + kStages;
   uint64_t* tmem_full = empty + kStages;  // [2]
-  uint64_t* tmem_empty = tmem_full + 2;   // [2]
+  uint64_t* tmem_empty = tmem_full + 2;   // [2] leader: both CTAs drained accumulator b
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_rank();
+  const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
   const int total = P.MB * P.NB * P.splits;
 
   if (threadIdx.x == 0) {
@@ -315,47 +393,50 @@ __global__ void __launch_bounds__(kThreads, 1) rns_kernel(const __grid_constant_
     }
     for (int b = 0; b < 2; ++b) {
       dev::mbar_init(&tmem_full[b], 1);
-      dev::mbar_init(&tmem_empty[b], kEpiWarps);
+      dev::mbar_init(&tmem_empty[b], 2 * kEpiWarps);
     }
     dev::fence_barrier_init();
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
         dev::smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
   }
   i8::fence_before();
-  __syncthreads();
+  cluster_sync();
   i8::fence_after();
   const uint32_t tbase = *tmem_slot;
 
   if (warp == 0) {
-    // ---------------- TMA producer ----------------
+    // ---------------- TMA producer (both CTAs: own A rows, own B columns) ----------------
+    // The leader's full[s] expects both CTAs' bytes; each CTA's loads
+    // complete on it, so the leader's one wait covers the pair.
     if (lane == 0) {
       int g = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      for (int t = pair; t < total; t += npairs) {
         const Item it = item_of(t, P);
         const int kb0 = it.ks * P.kb_per_split;
         const int nkb = max(0, min(P.KB, kb0 + P.kb_per_split) - kb0);
+        const i64 rb = 2 * static_cast<i64>(it.tm) + rank, cb = 2 * static_cast<i64>(it.tn) + rank;
         for (int i = 0; i < P.nmod; ++i) {
-          const uint8_t* gA = P.apack + ((static_cast<i64>(it.tm) * P.nmod + i) * P.KB + kb0) * kAStage;
-          const uint8_t* gB = P.bpack + ((static_cast<i64>(it.tn) * P.nmod + i) * P.KB + kb0) * kBStage;
+          const int rowA = static_cast<int>(((rb * P.nmod + i) * P.KB + kb0) * (kAStage / 128));
+          const int rowB = static_cast<int>(((cb * P.nmod + i) * P.KB + kb0) * (kBStage / 128));
           for (int kb = 0; kb < nkb; ++kb, ++g) {
             const int s = g % kStages;
             if (g >= kStages) dev::mbar_wait(&empty[s], ((g / kStages) - 1) & 1);
-            dev::mbar_arrive_expect_tx(&full[s], kStageBytes);
-            dev::bulk_g2s(sA + s * kAStage, gA + static_cast<i64>(kb) * kAStage, kAStage, &full[s]);
-            dev::bulk_g2s(sB + s * kBStage, gB + static_cast<i64>(kb) * kBStage, kBStage, &full[s]);
+            if (rank == 0) dev::mbar_arrive_expect_tx(&full[s], 2 * kStageBytes);
+            tma_pair_load(sA + s * kAStage, &P.tmA, rowA + kb * (kAStage / 128), &full[s]);
+            tma_pair_load(sB + s * kBStage, &P.tmB, rowB + kb * (kBStage / 128), &full[s]);
           }
         }
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer (one thread) ----------------
-    if (lane == 0) {
-      constexpr uint32_t idesc = i8::instr_desc(kBM, kNT);
+    if (rank == 0 && lane == 0) {
+      // ---------------- MMA issuer (leader CTA, one thread) ----------------
+      constexpr uint32_t idesc = i8::instr_desc(kPairM, kNT);
       int g = 0, pass = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      for (int t = pair; t < total; t += npairs) {
         const Item it = item_of(t, P);
         const int kb0 = it.ks * P.kb_per_split;
         const int nkb = max(0, min(P.KB, kb0 + P.kb_per_split) - kb0);
@@ -364,7 +445,7 @@ __global__ void __launch_bounds__(kThreads, 1) rns_kernel(const __grid_constant_
           int kb = 0;
           for (int seg = 0; seg < nseg; ++seg, ++pass) {
             const int b = pass & 1;
-            dev::mbar_wait(&tmem_empty[b], ((pass >> 1) & 1) ^ 1);
+            mbar_wait_cluster(&tmem_empty[b], ((pass >> 1) & 1) ^ 1);
             i8::fence_after();
             const uint32_t tacc = tbase + b * kNT;
             const int kend = min(nkb, kb + P.seg_kb);
@@ -377,25 +458,26 @@ __global__ void __launch_bounds__(kThreads, 1) rns_kernel(const __grid_constant_
 #pragma unroll
               for (int tk = 0; tk < kKSteps; ++tk) {
                 const uint64_t ad = i8::smem_desc(a0 + tk * 2 * (kBM / 8) * 128, (kBM / 8) * 128, 128);
-                const uint64_t bd = i8::smem_desc(b0 + tk * 2 * (kNT / 8) * 128, (kNT / 8) * 128, 128);
-                i8::mma_i8(tacc, ad, bd, idesc, (kb > kstart || tk > 0) ? 1u : 0u);
+                const uint64_t bd = i8::smem_desc(b0 + tk * 2 * (kBH / 8) * 128, (kBH / 8) * 128, 128);
+                mma_i8_pair(tacc, ad, bd, idesc, (kb > kstart || tk > 0) ? 1u : 0u);
               }
-              i8::mma_commit(&empty[s]);
+              commit_pair(&empty[s]);  // frees stage s in both CTAs
             }
-            i8::mma_commit(&tmem_full[b]);
+            commit_pair(&tmem_full[b]);  // accumulator b complete in both CTAs
           }
         }
       }
     }
   } else {
-    // ---------------- epilogue: warps 2..9 ----------------
+    // ---------------- epilogue: warps 2..9 of both CTAs ----------------
     const int quad = warp % 4;
     const int half = (warp - 2) / 4;
     const int row_in_tile = quad * 32 + lane;
     const uint32_t tlane = static_cast<uint32_t>(quad * 32) << 16;
+    const uint32_t leader_tmem_empty = peer_addr(tmem_empty, 0);
     uint8_t* slot = P.scratch + static_cast<i64>(blockIdx.x) * P.nmod * kSlotPerMod;
     int pass = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    for (int t = pair; t < total; t += npairs) {
       const Item it = item_of(t, P);
       const int kb0 = it.ks * P.kb_per_split;
       const int nkb = max(0, min(P.KB, kb0 + P.kb_per_split) - kb0);
@@ -415,7 +497,7 @@ __global__ void __launch_bounds__(kThreads, 1) rns_kernel(const __grid_constant_
             if (c0 + 32 == kNT / 2) {  // every column of this buffer is in registers: release it
               i8::fence_before();
               __syncwarp();
-              if (lane == 0) dev::mbar_arrive(&tmem_empty[b]);
+              if (lane == 0) mbar_arrive_cluster(leader_tmem_empty + b * 8);
             }
             park32(v, m, c16, mg, seg > 0, scratch_at(slot, i, half, c0 / 16, row_in_tile),
                    scratch_at(slot, i, half, c0 / 16 + 1, row_in_tile));
@@ -423,7 +505,7 @@ __global__ void __launch_bounds__(kThreads, 1) rns_kernel(const __grid_constant_
         }
       }
       // CRT over the parked residues of this thread's row / column half
-      const i64 row = static_cast<i64>(it.tm) * kBM + row_in_tile;
+      const i64 row = (2 * static_cast<i64>(it.tm) + rank) * kBM + row_in_tile;
       const i64 colh = static_cast<i64>(it.tn) * kNT + half * (kNT / 2);
       double* dst_row = P.C + static_cast<i64>(it.ks) * P.split_stride + row * P.ldc + colh;
 #pragma unroll 1
@@ -434,10 +516,10 @@ __global__ void __launch_bounds__(kThreads, 1) rns_kernel(const __grid_constant_
     }
   }
   i8::fence_before();
-  __syncthreads();
+  cluster_sync();
   if (warp == 1) {
     i8::fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
   }
 }
 

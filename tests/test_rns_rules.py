@@ -127,19 +127,20 @@ def test_magic_reduction_exhaustive_epilogue_range(m):
 
 
 def test_packer_residue_split():
-    """residues16(): x mod m from 18-bit limbs plus the centring offset."""
+    """residues16(): two dp4a over the base-256 digits of x, with the centring
+    flag [x > p/2] as a ninth 'digit' weighted by the residue of -p."""
     p = F.prev_prime(1 << 52)
     pl = F.rns_plan(p, 8192)
     rng = random.Random(7)
     xs = [0, 1, p // 2, p // 2 + 1, p - 1] + [rng.randrange(p) for _ in range(2000)]
     for m in pl["moduli"]:
-        c1, c2, na = (1 << 18) % m, (1 << 36) % m, (m - p % m) % m
+        w = [pow(256, j, m) for j in range(7)] + [(m - p % m) % m]
+        assert all(c < 256 for c in w)
         for x in xs:
-            x0, x1, x2 = x & 0x3FFFF, (x >> 18) & 0x3FFFF, x >> 36
-            neg = 1 if x > p // 2 else 0
-            s = x0 + x1 * c1 + x2 * c2 + neg * na
-            assert s < 1 << 27
-            centred = x - p if neg else x
+            d = [(x >> (8 * j)) & 0xFF for j in range(7)] + [1 if x > p // 2 else 0]
+            s = sum(a * b for a, b in zip(d, w))
+            assert s < 1 << 19
+            centred = x - p if x > p // 2 else x
             assert s % m == centred % m
 
 

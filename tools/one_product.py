@@ -19,7 +19,7 @@ F.random_residues_device(A, p, 1)
 F.random_residues_device(B, p, 2)
 for _ in range(reps):
     tm = F.Timing()
-    eng = {'i8': F.ENGINE_I8, 'dmma': F.ENGINE_DMMA}[os.environ.get('ENGINE', 'dmma')]
+    eng = {'i8': F.ENGINE_I8, 'dmma': F.ENGINE_DMMA, 'rns': F.ENGINE_RNS}[os.environ.get('ENGINE', 'dmma')]
     F.mw_product_device(A, B, C, p, pl.u, pl.v, pl.lambda_, timing=tm, flags=eng)
     print(bits, (pl.u, pl.v, pl.lambda_), tm.as_dict(),
           "eff %.1f GF/s, fp64 %.2f TF/s" % (2 * m * k * n / tm.gemm_ms / 1e6, 2 * pl.u * pl.v * m * k * n / tm.gemm_ms / 1e9))
