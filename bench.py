@@ -173,8 +173,9 @@ def main():
     ap.add_argument("--bits", default="20-52")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--engine", default="i8", choices=["i8", "dmma"],
-                    help="engine timed for `value`/`e2e` (both are recorded per bitsize)")
+    ap.add_argument("--engine", default="auto", choices=["auto", "i8", "rns", "dmma"],
+                    help="engine timed for `value`/`e2e` (auto = the library default; all are recorded per "
+                         "bitsize)")
     args = ap.parse_args()
     m, k, n, wl_bits = WORKLOADS[args.workload]
     bits_list = wl_bits if wl_bits is not None else parse_bits(args.bits)
@@ -228,7 +229,7 @@ def main():
     # cap, not the tensor pipe, bounds a long int8 step on this 1 kW part)
     peaks = {"dmma": F.fp64_peak(local), "i8_burst": F.i8_peak(local, 200000),
              "i8": F.i8_peak(local, 20000000)}
-    eng_flags = {"dmma": F.ENGINE_DMMA, "i8": F.ENGINE_I8}
+    eng_flags = {"dmma": F.ENGINE_DMMA, "i8": F.ENGINE_I8, "rns": F.ENGINE_RNS, "auto": 0}
     # one non-default stream carries every product and the timing events
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
@@ -249,7 +250,7 @@ def main():
                                     timing=tm if record is not None else None)
                 launches[0] += (2 if rn else 0) + (1 if rank == 0 else 0)
             if record is not None:
-                record[b] = tm.gemm_ms
+                record[b] = (tm.gemm_ms, tm.engine, tm.words)
 
     def barrier():
         if world > 1:
@@ -289,47 +290,57 @@ def main():
         except Exception:
             traffic_db = {}
     engines = {}
-    for eng in ("i8", "dmma"):
+    kernel_desc = {
+        F.ENGINE_DMMA: "mwgemm_kernel: DMMA.8x8x4 FP64 tensor pipe; work = 2uv*mnk FP64 flops",
+        F.ENGINE_I8: "mwi8_kernel: tcgen05.mma.kind::i8 (UTCIMMA), TMEM int32; work = 2*D^2*mnk int8 tensor "
+                     "ops (D base-256 digits)",
+        F.ENGINE_RNS: "rns_kernel: tcgen05.mma.cta_group::2.kind::i8 (UTCIMMA.2CTA) M256 N256, TMEM int32, fused "
+                      "CRT epilogue; work = 2*n_mod*mnk int8 tensor ops (n_mod byte moduli)",
+    }
+    for eng in ("auto", "i8", "rns", "dmma"):
         rec = {}
         step(eng, record=rec)
         torch.cuda.synchronize()
         per_bits = {}
         work = gemm_total = 0.0
+        ran = set()
         for (b, p, u, v, lam, lk) in probs:
-            g = rec[b]
+            g, e_ran, words = rec[b]
+            ran.add(e_ran)
             rn = rows[b][1]
-            if eng == "dmma":
+            if e_ran == F.ENGINE_DMMA:
                 w = 2.0 * u * v * rn * k * n           # uv-scaled FP64 work
                 extra = {"lambda_k": lk}
+            elif e_ran == F.ENGINE_I8:
+                w = 2.0 * words * words * rn * k * n   # D^2 int8 digit products
+                extra = {"engine": "i8", "digits": words}
             else:
-                d = max(1, ((p - 1).bit_length() + 7) // 8)
-                w = 2.0 * d * d * rn * k * n           # D^2 int8 word products
-                extra = {"digits": d}
+                w = 2.0 * words * rn * k * n           # one int8 GEMM per byte modulus
+                extra = {"engine": "rns", "moduli": words}
             work += w
             gemm_total += g
+            pk = "dmma" if e_ran == F.ENGINE_DMMA else "i8"
             per_bits[str(b)] = dict({"u": u, "v": v, "lambda": lam, "gemm_ms": round(g, 3),
                                      "eff_gflops": round(2.0 * rn * k * n / (g * 1e-3) / 1e9, 1),
-                                     "tensor_frac": round(w / (g * 1e-3) / 1e12 / peaks[eng], 4)}, **extra)
+                                     "tensor_frac": round(w / (g * 1e-3) / 1e12 / peaks[pk], 4)}, **extra)
         achieved = work / (gemm_total * 1e-3) / 1e12
+        pk = "dmma" if eng == "dmma" else "i8"
         tr = traffic_db.get(eng, {})
         engines[eng] = {
             "eff_gflops": round(flops_step / (gemm_total * 1e-3) / 1e9, 1),
-            "roofline": {"bound": "tensor", "achieved": round(achieved, 3), "peak": round(peaks[eng], 3),
-                         "unit": "TFLOP/s", "frac": round(achieved / peaks[eng], 4),
+            "roofline": {"bound": "tensor", "achieved": round(achieved, 3), "peak": round(peaks[pk], 3),
+                         "unit": "TFLOP/s", "frac": round(achieved / peaks[pk], 4),
                          "traffic": tr.get("dram_bytes_per_launch"),
-                         "kernel": ("mwgemm_kernel: DMMA.8x8x4 FP64 tensor pipe; work = 2uv*mnk FP64 flops"
-                                    if eng == "dmma" else
-                                    "mwi8_kernel: tcgen05.mma.kind::i8 (UTCIMMA), TMEM int32; work = 2*D^2*mnk "
-                                    "int8 tensor ops (reported as TFLOP/s = T int8-op/s)"),
+                         "kernel": " + ".join(kernel_desc[e] for e in sorted(ran)),
                          "peak_source": ("measured DMMA-only loop on this GPU (MEASURED_PEAKS.json has no FP64 "
-                                         "entry); vendor FP64 tensor 37.2 TF @1965 MHz" if eng == "dmma" else
+                                         "entry); vendor FP64 tensor 37.2 TF @1965 MHz" if pk == "dmma" else
                                          "measured SUSTAINED rate of back-to-back tcgen05 kind::i8 M128 N256 "
                                          "K32 MMAs on random operands, all SMs, 1.4 s under the 1 kW power cap "
                                          "(the kernel is timed inside a long step; MEASURED_PEAKS.json has no "
                                          "int8 entry); burst %.0f TOP/s, vendor dense int8 4.5 POPS"
                                          % peaks["i8_burst"])},
             "sweep": per_bits}
-        if eng == "i8":
+        if pk == "i8":
             engines[eng]["roofline"]["frac_of_burst_peak"] = round(achieved / peaks["i8_burst"], 4)
     roof = dict(engines[args.engine]["roofline"])
     # end to end through the public host-buffer API (pinned memory), one step

@@ -51,7 +51,8 @@ typedef enum {
  *   I8  : base-256 multiword words on tcgen05.mma.kind::i8 (int32 TMEM accumulators)
  *   RNS : byte residues modulo pairwise-coprime m_i <= 256, one kind::i8 GEMM per
  *         modulus, CRT reconstruction mod p fused into the epilogue
- * no flag = the library default (I8) */
+ * no flag = the library default: I8 or RNS, whichever a B200 time model
+ * predicts faster for (m, k, n, p) (I8 for prepared A, where n is unknown) */
 #define FPMM_B200_ENGINE_DMMA 0x10u
 #define FPMM_B200_ENGINE_I8 0x20u
 #define FPMM_B200_ENGINE_RNS 0x40u
@@ -84,6 +85,8 @@ typedef struct {
   int64_t lambda_k;    /* K-block between in-register reductions (terms)     */
   int32_t launches;    /* kernels launched by this call (all devices)        */
   int32_t ngpus;       /* devices used                                       */
+  int32_t engine;      /* engine that ran: 0x10 DMMA, 0x20 I8, 0x40 RNS (FPMM_B200_ENGINE_*) */
+  int32_t words;       /* words per residue: u*v (DMMA), base-256 digits D (I8), moduli (RNS) */
 } fpmm_b200_timing;
 
 /* ------------------------------------------------------------ diagnostics */

@@ -80,7 +80,7 @@ _default_engine_flags = 0
 
 def set_default_engine(name: Optional[str]) -> None:
     """Engine used when a call passes no ENGINE_* flag: "i8", "rns", "dmma" or
-    None (the library default)."""
+    None (the library default: i8 or rns by a per-shape time model)."""
     global _default_engine_flags
     _default_engine_flags = {"i8": ENGINE_I8, "rns": ENGINE_RNS, "dmma": ENGINE_DMMA, None: 0}[name]
 
@@ -99,7 +99,8 @@ class Timing(C.Structure):
     """fpmm_b200_timing: CUDA-event phase times of one call (ms)."""
     _fields_ = [("h2d_ms", C.c_double), ("pack_ms", C.c_double), ("gemm_ms", C.c_double),
                 ("comm_ms", C.c_double), ("d2h_ms", C.c_double), ("total_ms", C.c_double),
-                ("lambda_k", C.c_int64), ("launches", C.c_int32), ("ngpus", C.c_int32)]
+                ("lambda_k", C.c_int64), ("launches", C.c_int32), ("ngpus", C.c_int32),
+                ("engine", C.c_int32), ("words", C.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -27,7 +27,7 @@ import time
 
 import numpy as np
 
-from . import (ENGINE_DMMA, ENGINE_I8, Error, FpContext, InfeasibleError, Timing, kVariants,
+from . import (ENGINE_DMMA, ENGINE_I8, ENGINE_RNS, Error, FpContext, InfeasibleError, Timing, kVariants,
                matrix_seed, mw_block_size, plan_for_modulus, prev_prime, random_mat,
                variant_admits_bits)
 
@@ -35,7 +35,7 @@ SCHEMA_VERSION = 1
 HEADER = ["schema_version", "scenario", "m", "k", "n", "bits", "p", "u", "v", "concat", "lambda",
           "kernel", "runs", "t_avg_s", "eff_gflops", "status"]
 EXTENDED = ["engine", "lambda_k", "gpus", "device_ms"]
-KERNELS = {"b200": 0, "b200-i8": ENGINE_I8, "b200-dmma": ENGINE_DMMA}
+KERNELS = {"b200": 0, "b200-i8": ENGINE_I8, "b200-rns": ENGINE_RNS, "b200-dmma": ENGINE_DMMA}
 
 
 def preset_dims(scenario: str, scale: float):
@@ -133,7 +133,8 @@ def run_bench(args) -> list:
                 rec["lambda"] = lam_used
                 rec["t_avg_s"] = total / args.runs
                 rec["eff_gflops"] = effective_gflops(m, k, n, rec["t_avg_s"])
-                rec["engine"] = "i8" if (flags or ENGINE_I8) & ENGINE_I8 else "dmma"
+                rec["engine"] = ("rns" if flags & ENGINE_RNS else "dmma" if flags & ENGINE_DMMA
+                                 else "i8" if flags & ENGINE_I8 else "auto")
                 rec["lambda_k"] = tm.lambda_k
                 rec["device_ms"] = dev / args.runs
                 if prepared is not None:

@@ -7,6 +7,7 @@
 #include "nccl_loader.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -152,7 +153,7 @@ int grid_for(i64 items, int threads) {
 }
 
 // Everything the kernels need for one (m, k, n, p, u, v) problem.
-enum Engine { kDmma = 0, kI8 = 1, kRns = 2 };
+enum Engine { kDmma = 0, kI8 = 1, kRns = 2, kAuto = 3 };
 
 struct Job {
   i64 m, k, n;
@@ -185,11 +186,38 @@ void dispatch_d(int D, F&& f) {
   throw Failure(FPMM_B200_EERROR, "int8 engine: unsupported digit count " + std::to_string(D));
 }
 
+int engine_flag(const Job& j) {
+  return j.engine == kRns ? FPMM_B200_ENGINE_RNS : j.engine == kI8 ? FPMM_B200_ENGINE_I8 : FPMM_B200_ENGINE_DMMA;
+}
+int engine_words(const Job& j) { return j.engine == kRns ? j.nmod : j.engine == kI8 ? j.D : j.u * j.v; }
+
 int resolve_engine(unsigned flags) {
   if (flags & FPMM_B200_ENGINE_RNS) return kRns;
   if (flags & FPMM_B200_ENGINE_I8) return kI8;
   if (flags & FPMM_B200_ENGINE_DMMA) return kDmma;
-  return kI8;  // library default: the int8 tcgen05 engine (same results, ~5-13x faster)
+  return kAuto;  // library default: the faster tcgen05 engine for the shape (same results)
+}
+
+// The library default between the two tcgen05 engines, by a time model fitted
+// on B200 (8192^3, profiles/round1): the base-256 engine costs D^2 int8 GEMMs
+// on NT-column tiles, the RNS engine n_mod GEMMs on 256 x 256 pair tiles
+// (~12% less efficient each) and packs n_mod instead of D bytes per element.
+int auto_engine(i64 m, i64 k, i64 n, u64 p) {
+  const int D = std::max(1, (bitsize(p - 1) + 7) / 8);
+  int nmod = 0;
+  try {
+    nmod = rns_plan(p, k).n;
+  } catch (const Failure&) {
+    return kI8;
+  }
+  int nt = 32;
+  dispatch_d(D, [&]<int DD>() { nt = i8::Cfg<DD>::kNT; });
+  const double mk_kn = static_cast<double>(m) * k + static_cast<double>(k) * n;
+  const double n_i8 = static_cast<double>((n + nt - 1) / nt * nt);
+  const double n_rns = static_cast<double>((n + 255) / 256 * 256), m_rns = static_cast<double>((m + 255) / 256 * 256);
+  const double t_i8 = D * D * 2.0 * m * k * n_i8 / 3.2e15 + (8.0 + D) * mk_kn / 4.5e12;
+  const double t_rns = nmod * 2.0 * m_rns * k * n_rns / 2.8e15 + (8.0 + nmod) * mk_kn / 3.0e12;
+  return t_rns < t_i8 ? kRns : kI8;
 }
 
 Job make_i8_job(i64 m, i64 k, i64 n, u64 p) {
@@ -280,6 +308,7 @@ Job make_rns_job(i64 m, i64 k, i64 n, u64 p) {
 }
 
 Job make_job(i64 m, i64 k, i64 n, u64 p, int u, int v, int engine = kDmma) {
+  if (engine == kAuto) engine = auto_engine(m, k, n, p);
   if (engine == kRns) {
     Job j = make_rns_job(m, k, n, p);
     j.u = u, j.v = v;
@@ -487,6 +516,9 @@ void launch_gemm_rns(const Job& j, const void* apack, const void* bpack, double*
   q.bpack = static_cast<const uint8_t*>(bpack);
   q.tmA = chunk_map(apack, static_cast<size_t>((rows + rns::kPairM - 1) / rns::kPairM) * j.per_rb_bytes);
   q.tmB = chunk_map(bpack, j.bpack_bytes);
+  if (const char* d = std::getenv("FPMM_B200_RNS_DEBUG")) q.dbg = std::atoi(d);
+  q.group = rns::kGroup;
+  if (const char* d = std::getenv("FPMM_B200_RNS_GROUP")) q.group = std::max(1, std::atoi(d));
   q.C = C;
   q.ldc = ldc;
   q.m = rows;
@@ -521,7 +553,9 @@ void launch_gemm_rns(const Job& j, const void* apack, const void* bpack, double*
   if (items > 0x7fffffff) throw Failure(FPMM_B200_EERROR, "problem too large for one launch");
   // persistent CTA pairs (clusters of 2 on neighbouring SMs)
   const unsigned grid = 2 * static_cast<unsigned>(std::max<i64>(1, std::min<i64>(items, sms / 2)));
-  q.scratch = static_cast<uint8_t*>(dc.scratch.get(static_cast<size_t>(grid) * j.nmod * rns::kSlotPerMod));
+  // residue bytes of every item (modulus-major order: a tile's CRT runs in
+  // the pass of its last modulus), n bytes per output element
+  q.scratch = static_cast<uint8_t*>(dc.scratch.get(static_cast<size_t>(items) * 2 * j.nmod * rns::kSlotPerMod));
   static bool configured[64] = {};
   if (!configured[dev & 63]) {
     CUDA_OK(cudaFuncSetAttribute(rns::rns_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, rns::kSmem));
@@ -642,6 +676,7 @@ void product_device(const ProductArgs& a, int device, void* stream, fpmm_b200_ti
     tm->gemm_ms = elapsed(c.ev[1], c.ev[2]);
     tm->total_ms = elapsed(c.ev[0], c.ev[2]);
     tm->lambda_k = j.lambda_k;
+    tm->engine = engine_flag(j), tm->words = engine_words(j);
     tm->launches = 3;
     tm->ngpus = 1;
   }
@@ -671,6 +706,9 @@ Prepared* prepare_a_device(const double* dA, i64 lda, i64 m, i64 k, u64 p, int u
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c.stream;
   auto h = std::make_unique<Prepared>();
   h->device = device, h->engine = resolve_engine(flags), h->p = p, h->u = u, h->v = v, h->m = m, h->k = k;
+  // n is unknown when A is prepared; the resident-A (unbalanced) scenario
+  // multiplies by narrow B blocks, where the base-256 engine's narrow tiles win
+  if (h->engine == kAuto) h->engine = kI8;
   h->flags = flags;
   if (m > 0 && k > 0) {
     const Job j = make_job(m, k, 1, p, u, v, h->engine);
@@ -733,6 +771,7 @@ void product_prepared_device(const Prepared* h, const double* dB, i64 ldb, doubl
     tm->gemm_ms = elapsed(c.ev[1], c.ev[2]);
     tm->total_ms = elapsed(c.ev[0], c.ev[2]);
     tm->lambda_k = j.lambda_k;
+    tm->engine = engine_flag(j), tm->words = engine_words(j);
     tm->launches = 2;
     tm->ngpus = 1;
   }
@@ -841,6 +880,7 @@ void product_host(const ProductArgs& a, int ngpus, fpmm_b200_timing* tm) {
       tm->d2h_ms = elapsed(c.ev_out[nch - 1], c.ev[3]);  // exposed tail of the D2H
       tm->total_ms = elapsed(c.ev[0], c.ev[3]);
       tm->lambda_k = j.lambda_k;
+    tm->engine = engine_flag(j), tm->words = engine_words(j);
       tm->launches = 1 + 2 * nch;
       tm->ngpus = 1;
     }
@@ -921,6 +961,7 @@ void product_host(const ProductArgs& a, int ngpus, fpmm_b200_timing* tm) {
     tm->h2d_ms = h2d, tm->pack_ms = pack, tm->comm_ms = comm, tm->gemm_ms = gemm, tm->d2h_ms = d2h;
     tm->total_ms = total;
     tm->lambda_k = j.lambda_k;
+    tm->engine = engine_flag(j), tm->words = engine_words(j);
     tm->launches = 2 * ngpus + 1;
     tm->ngpus = ngpus;
   }
@@ -1167,10 +1208,10 @@ void dist_finalize() {
 
 void dist_rows(i64 m, int nranks, int rank, int u, int v, i64* row0, i64* rows) {
   if (nranks < 1 || rank < 0 || rank >= nranks) throw Failure(FPMM_B200_EERROR, "dist_rows: bad rank/size");
-  // 128 = a multiple of every engine's CTA row tile (DMMA BM in {32,64,128},
-  // int8 BM = 128), so each rank packs whole tiles whatever the engine
+  // 256 = a multiple of every engine's row tile (DMMA BM in {32,64,128},
+  // int8 BM = 128, RNS pair tile 256), so each rank packs whole tiles whatever the engine
   dispatch(u, v, [&]<int U, int V, int MT, int NT>() {});  // rejects unsupported (u,v)
-  const i64 per = part_rows(m, nranks, 128);
+  const i64 per = part_rows(m, nranks, 256);
   const i64 r0 = std::min<i64>(m, rank * per);
   *row0 = r0;
   *rows = std::min<i64>(m, r0 + per) - r0;
@@ -1242,6 +1283,7 @@ void dist_product_device(const double* dA_rows, i64 lda, const double* dB, i64 l
     tm->gemm_ms = elapsed(c.ev[2], c.ev[3]);
     tm->total_ms = elapsed(c.ev[0], c.ev[4]);
     tm->lambda_k = j.lambda_k;
+    tm->engine = engine_flag(j), tm->words = engine_words(j);
     tm->launches = launches;
     tm->ngpus = g_dist.nranks;
   }

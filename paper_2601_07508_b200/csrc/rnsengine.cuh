@@ -64,13 +64,15 @@ struct Params {
   const uint8_t* apack;  // [128-row block][modulus][k-block] chunks of kAStage bytes
   const uint8_t* bpack;  // [128-column block][modulus][k-block] chunks of kBStage bytes
   double* C;
-  uint8_t* scratch;      // per CTA: nmod * kSlotPerMod bytes
+  uint8_t* scratch;      // residue blocks: [item][CTA rank] x nmod * kSlotPerMod bytes
   i64 ldc, m, n;
   int MB, NB, KB;    // pair tiles (256 x 256) along m and n; 64-byte k-blocks
   int nmod;
   int seg_kb;        // k-blocks per exact int32 segment
   int kb_per_split;  // split-K: k-blocks per slice
   int splits;
+  int group;         // pair-tile rows per rasterisation group
+  int dbg;           // experiments only (FPMM_B200_RNS_DEBUG): 1 = L2-resident operands, 2 = empty epilogue
   i64 split_stride;
   unsigned long long p, mu;            // Barrett: mu = floor(2^64 / p)
   unsigned long long two32, two32_sh;  // 2^32 mod p and its Shoup quotient
@@ -211,9 +213,9 @@ struct Item {
 __device__ __forceinline__ Item item_of(int t, const Params& P) {
   const int tiles = P.MB * P.NB;
   const int r = t % tiles;
-  const int in_group = kGroup * P.NB;
-  const int first_m = (r / in_group) * kGroup;
-  const int gsz = min(P.MB - first_m, kGroup);
+  const int in_group = P.group * P.NB;
+  const int first_m = (r / in_group) * P.group;
+  const int gsz = min(P.MB - first_m, P.group);
   Item it;
   it.tm = first_m + (r % in_group) % gsz;
   it.tn = (r % in_group) / gsz;
@@ -267,25 +269,31 @@ __device__ __forceinline__ void park32(const uint32_t (&v)[32], uint32_t m, uint
 }
 
 // CRT of 8 columns (half `sub` of a 16-byte residue row) of one row -> C.
+// All nmod residue words are loaded before any is used, so the parked bytes
+// (possibly evicted to HBM by the time the tile ends) cost one round trip.
 __device__ __forceinline__ void crt8(const Params& P, uint8_t* slot, int half, int c16, int sub, int row_in_tile,
                                      i64 row, i64 col0, double* dst) {
+  uint2 rw[kMaxMod];
+#pragma unroll
+  for (int i = 0; i < kMaxMod; ++i)
+    if (i < P.nmod) rw[i] = reinterpret_cast<const uint2*>(scratch_at(slot, i, half, c16, row_in_tile))[sub];
+  if (row >= P.m) return;
   unsigned long long s_lo[8], s_hi[8], f[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) s_lo[e] = s_hi[e] = f[e] = 0;
-#pragma unroll 2
-  for (int i = 0; i < P.nmod; ++i) {
-    const uint4 r4 = *scratch_at(slot, i, half, c16, row_in_tile);
-    const uint32_t rw[2] = {sub ? r4.z : r4.x, sub ? r4.w : r4.y};
+#pragma unroll
+  for (int i = 0; i < kMaxMod; ++i) {
+    if (i >= P.nmod) break;
+    const uint32_t w2[2] = {rw[i].x, rw[i].y};
     const uint32_t wl = P.w_lo[i], wh = P.w_hi[i], g = P.g[i];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      const uint32_t r = (rw[e / 4] >> (8 * (e % 4))) & 0xFFu;
+      const uint32_t r = (w2[e / 4] >> (8 * (e % 4))) & 0xFFu;
       s_lo[e] += static_cast<unsigned long long>(r) * wl;
       s_hi[e] += static_cast<unsigned long long>(r) * wh;
       f[e] += static_cast<unsigned long long>(r) * g;
     }
   }
-  if (row >= P.m) return;
   const unsigned long long p = P.p;
   double out[8];
 #pragma unroll
@@ -413,20 +421,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
     // complete on it, so the leader's one wait covers the pair.
     if (lane == 0) {
       int g = 0;
-      for (int t = pair; t < total; t += npairs) {
-        const Item it = item_of(t, P);
-        const int kb0 = it.ks * P.kb_per_split;
-        const int nkb = max(0, min(P.KB, kb0 + P.kb_per_split) - kb0);
-        const i64 rb = 2 * static_cast<i64>(it.tm) + rank, cb = 2 * static_cast<i64>(it.tn) + rank;
-        for (int i = 0; i < P.nmod; ++i) {
-          const int rowA = static_cast<int>(((rb * P.nmod + i) * P.KB + kb0) * (kAStage / 128));
-          const int rowB = static_cast<int>(((cb * P.nmod + i) * P.KB + kb0) * (kBStage / 128));
+      for (int i = 0; i < P.nmod; ++i) {
+        for (int t = pair; t < total; t += npairs) {
+          const Item it = item_of(t, P);
+          const int kb0 = it.ks * P.kb_per_split;
+          const int nkb = max(0, min(P.KB, kb0 + P.kb_per_split) - kb0);
+          const i64 rb = 2 * static_cast<i64>(it.tm) + rank, cb = 2 * static_cast<i64>(it.tn) + rank;
+          int rowA = static_cast<int>(((rb * P.nmod + i) * P.KB + kb0) * (kAStage / 128));
+          int rowB = static_cast<int>(((cb * P.nmod + i) * P.KB + kb0) * (kBStage / 128));
+          if (P.dbg & 1) rowA = rowB = static_cast<int>(rank) * 64 * 32;
           for (int kb = 0; kb < nkb; ++kb, ++g) {
             const int s = g % kStages;
             if (g >= kStages) dev::mbar_wait(&empty[s], ((g / kStages) - 1) & 1);
             if (rank == 0) dev::mbar_arrive_expect_tx(&full[s], 2 * kStageBytes);
-            tma_pair_load(sA + s * kAStage, &P.tmA, rowA + kb * (kAStage / 128), &full[s]);
-            tma_pair_load(sB + s * kBStage, &P.tmB, rowB + kb * (kBStage / 128), &full[s]);
+            const int kq = (P.dbg & 1) ? (kb & 31) : kb;
+            tma_pair_load(sA + s * kAStage, &P.tmA, rowA + kq * (kAStage / 128), &full[s]);
+            tma_pair_load(sB + s * kBStage, &P.tmB, rowB + kq * (kBStage / 128), &full[s]);
           }
         }
       }
@@ -436,12 +446,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
       // ---------------- MMA issuer (leader CTA, one thread) ----------------
       constexpr uint32_t idesc = i8::instr_desc(kPairM, kNT);
       int g = 0, pass = 0;
-      for (int t = pair; t < total; t += npairs) {
-        const Item it = item_of(t, P);
-        const int kb0 = it.ks * P.kb_per_split;
-        const int nkb = max(0, min(P.KB, kb0 + P.kb_per_split) - kb0);
-        const int nseg = max(1, (nkb + P.seg_kb - 1) / P.seg_kb);
-        for (int i = 0; i < P.nmod; ++i) {
+      for (int i = 0; i < P.nmod; ++i) {
+        for (int t = pair; t < total; t += npairs) {
+          const Item it = item_of(t, P);
+          const int kb0 = it.ks * P.kb_per_split;
+          const int nkb = max(0, min(P.KB, kb0 + P.kb_per_split) - kb0);
+          const int nseg = max(1, (nkb + P.seg_kb - 1) / P.seg_kb);
           int kb = 0;
           for (int seg = 0; seg < nseg; ++seg, ++pass) {
             const int b = pass & 1;
@@ -470,20 +480,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
     }
   } else {
     // ---------------- epilogue: warps 2..9 of both CTAs ----------------
+    // Pass (modulus i, tile t): T_i mod m_i is parked in the tile's residue
+    // block in HBM; the pass of the last modulus then reads the tile's n
+    // residue bytes per element back and runs the CRT into C.  Each thread
+    // only ever reads bytes it wrote itself.
     const int quad = warp % 4;
     const int half = (warp - 2) / 4;
     const int row_in_tile = quad * 32 + lane;
     const uint32_t tlane = static_cast<uint32_t>(quad * 32) << 16;
     const uint32_t leader_tmem_empty = peer_addr(tmem_empty, 0);
-    uint8_t* slot = P.scratch + static_cast<i64>(blockIdx.x) * P.nmod * kSlotPerMod;
     int pass = 0;
-    for (int t = pair; t < total; t += npairs) {
-      const Item it = item_of(t, P);
-      const int kb0 = it.ks * P.kb_per_split;
-      const int nkb = max(0, min(P.KB, kb0 + P.kb_per_split) - kb0);
-      const int nseg = max(1, (nkb + P.seg_kb - 1) / P.seg_kb);
-      for (int i = 0; i < P.nmod; ++i) {
-        const uint32_t m = P.mod[i], c16 = P.c16[i], mg = P.magic[i];
+    for (int i = 0; i < P.nmod; ++i) {
+      const uint32_t m = P.mod[i], c16 = P.c16[i], mg = P.magic[i];
+      for (int t = pair; t < total; t += npairs) {
+        const Item it = item_of(t, P);
+        const int kb0 = it.ks * P.kb_per_split;
+        const int nkb = max(0, min(P.KB, kb0 + P.kb_per_split) - kb0);
+        const int nseg = max(1, (nkb + P.seg_kb - 1) / P.seg_kb);
+        uint8_t* slot = P.scratch + (static_cast<i64>(t) * 2 + rank) * P.nmod * kSlotPerMod;
         for (int seg = 0; seg < nseg; ++seg, ++pass) {
           const int b = pass & 1;
           dev::mbar_wait(&tmem_full[b], (pass >> 1) & 1);
@@ -499,19 +513,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
               __syncwarp();
               if (lane == 0) mbar_arrive_cluster(leader_tmem_empty + b * 8);
             }
-            park32(v, m, c16, mg, seg > 0, scratch_at(slot, i, half, c0 / 16, row_in_tile),
-                   scratch_at(slot, i, half, c0 / 16 + 1, row_in_tile));
+            if (!(P.dbg & 10))
+              park32(v, m, c16, mg, seg > 0, scratch_at(slot, i, half, c0 / 16, row_in_tile),
+                     scratch_at(slot, i, half, c0 / 16 + 1, row_in_tile));
           }
         }
-      }
-      // CRT over the parked residues of this thread's row / column half
-      const i64 row = (2 * static_cast<i64>(it.tm) + rank) * kBM + row_in_tile;
-      const i64 colh = static_cast<i64>(it.tn) * kNT + half * (kNT / 2);
-      double* dst_row = P.C + static_cast<i64>(it.ks) * P.split_stride + row * P.ldc + colh;
+        if (i + 1 == P.nmod && !(P.dbg & 6)) {
+          // CRT over the tile's parked residues of this thread's row / column half
+          const i64 row = (2 * static_cast<i64>(it.tm) + rank) * kBM + row_in_tile;
+          const i64 colh = static_cast<i64>(it.tn) * kNT + half * (kNT / 2);
+          double* dst_row = P.C + static_cast<i64>(it.ks) * P.split_stride + row * P.ldc + colh;
 #pragma unroll 1
-      for (int c = 0; c < (kNT / 2) / 8; ++c) {
-        if (colh + c * 8 >= P.n) break;
-        crt8(P, slot, half, c / 2, c % 2, row_in_tile, row, colh + c * 8, dst_row + c * 8);
+          for (int c = 0; c < (kNT / 2) / 8; ++c) {
+            if (colh + c * 8 >= P.n) break;
+            crt8(P, slot, half, c / 2, c % 2, row_in_tile, row, colh + c * 8, dst_row + c * 8);
+          }
+        }
       }
     }
   }

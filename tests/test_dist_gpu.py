@@ -21,7 +21,7 @@ def _port():
     return port
 
 
-@pytest.mark.parametrize("engine", ["i8", "dmma"])
+@pytest.mark.parametrize("engine", ["i8", "rns", "dmma"])
 def test_dist_world1_gather(engine):
     import torch
     import torch.distributed as td
@@ -39,7 +39,7 @@ def test_dist_world1_gather(engine):
         dB = torch.from_numpy(B).cuda()
         dCr = torch.empty((rn, n), dtype=torch.float64, device="cuda")
         dCf = torch.empty((m, n), dtype=torch.float64, device="cuda")
-        eng = F.ENGINE_I8 if engine == "i8" else F.ENGINE_DMMA
+        eng = {"i8": F.ENGINE_I8, "rns": F.ENGINE_RNS, "dmma": F.ENGINE_DMMA}[engine]
         tm = F.Timing()
         D.mw_product_device(dA, dB, dCr, p, pl.u, pl.v, pl.lambda_, m, root=0, C_full=dCf, flags=eng,
                             timing=tm)

@@ -14,10 +14,11 @@ import paper_2601_07508_b200 as F
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True, params=["dmma", "i8"])
+@pytest.fixture(autouse=True, params=["dmma", "i8", "rns", None])
 def engine(request):
-    """Every test runs on both engines: the FP64 DMMA multiword engine and the
-    int8 tcgen05 multiword engine (the library default)."""
+    """Every test runs on every engine: the FP64 DMMA multiword engine, the
+    base-256 int8 tcgen05 engine, the RNS int8 tcgen05 engine and the library
+    default (None: per-shape choice between the two tcgen05 engines)."""
     F.set_default_engine(request.param)
     yield request.param
     F.set_default_engine(None)
@@ -62,9 +63,10 @@ def test_config1_checksum(engine):
     assert C[0, 0] == 247707968029641 and C[-1, -1] == 526583644345359
     assert (C == O.exact_mod_gemm(A, B, p)).all()
     assert tm.launches == 3
-    # exact K-block between reductions: 28 terms (DMMA, signed words) or an
-    # int32 segment of 147 x 64 terms (int8, 7 digits)
-    assert tm.lambda_k == (28 if engine == "dmma" else 9408)
+    # exact K-block between reductions: 28 terms (DMMA, signed words), an
+    # int32 segment of 147 x 64 terms (base-256, 7 digits) or 1032 x 64 (RNS)
+    want = {"dmma": (28,), "i8": (9408,), "rns": (66048,), None: (9408, 66048)}[engine]
+    assert tm.lambda_k in want
 
 
 @pytest.mark.parametrize("u,v", COMBOS)

@@ -37,7 +37,7 @@ def run(name, engine, stream):
     C = torch.empty((m, n), dtype=torch.float64, device="cuda")
     F.random_residues_device(A, p, F.matrix_seed(1, bits, m, k, n, 0xA))
     F.random_residues_device(B, p, F.matrix_seed(1, bits, m, k, n, 0xB))
-    fl = F.ENGINE_I8 if engine == "i8" else F.ENGINE_DMMA
+    fl = {"i8": F.ENGINE_I8, "rns": F.ENGINE_RNS, "dmma": F.ENGINE_DMMA, "auto": 0}[engine]
     pa = F.PreparedA(A, p, pl.u, pl.v, flags=fl) if name == "unbalanced" else None
 
     def once(tm=None):
