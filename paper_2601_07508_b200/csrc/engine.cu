@@ -199,9 +199,10 @@ int resolve_engine(unsigned flags) {
 }
 
 // The library default between the two tcgen05 engines, by a time model fitted
-// on B200 (8192^3, profiles/round1): the base-256 engine costs D^2 int8 GEMMs
-// on NT-column tiles, the RNS engine n_mod GEMMs on 256 x 256 pair tiles
-// (~12% less efficient each) and packs n_mod instead of D bytes per element.
+// on B200 (8192^3 sweep, profiles/round1/bench_sweep8192.json): the base-256
+// engine costs D^2 int8 GEMMs on NT-column tiles, the RNS engine n_mod GEMMs
+// on 256 x 256 pair tiles (about the same time each) and packs n_mod instead
+// of D bytes per element.
 int auto_engine(i64 m, i64 k, i64 n, u64 p) {
   const int D = std::max(1, (bitsize(p - 1) + 7) / 8);
   int nmod = 0;
@@ -216,7 +217,7 @@ int auto_engine(i64 m, i64 k, i64 n, u64 p) {
   const double n_i8 = static_cast<double>((n + nt - 1) / nt * nt);
   const double n_rns = static_cast<double>((n + 255) / 256 * 256), m_rns = static_cast<double>((m + 255) / 256 * 256);
   const double t_i8 = D * D * 2.0 * m * k * n_i8 / 3.2e15 + (8.0 + D) * mk_kn / 4.5e12;
-  const double t_rns = nmod * 2.0 * m_rns * k * n_rns / 2.8e15 + (8.0 + nmod) * mk_kn / 3.0e12;
+  const double t_rns = nmod * 2.0 * m_rns * k * n_rns / 3.2e15 + (8.0 + nmod) * mk_kn / 3.0e12;
   return t_rns < t_i8 ? kRns : kI8;
 }
 
