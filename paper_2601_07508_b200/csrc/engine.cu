@@ -291,7 +291,8 @@ Job make_rns_job(i64 m, i64 k, i64 n, u64 p) {
     const u64 mi = pl.mod[i];
     q.mod[i] = pp.mod[i] = static_cast<uint32_t>(mi);
     q.c16[i] = static_cast<uint32_t>((u64{1} << 16) % mi);
-    q.magic[i] = pp.magic[i] = static_cast<uint32_t>(((u64{1} << 37) + mi - 1) / mi);
+    q.magic[i] = pp.magic[i] = static_cast<uint32_t>(((u64{1} << 32) + mi - 1) / mi);
+    q.negm[i] = pp.negm[i] = static_cast<uint32_t>(0u - static_cast<uint32_t>(mi));
     q.g[i] = pl.g[i];
     q.w_lo[i] = static_cast<uint32_t>(pl.W[i]);
     q.w_hi[i] = static_cast<uint32_t>(pl.W[i] >> 32);

@@ -112,18 +112,16 @@ def test_device_crt_reconstruction_at_the_range_extremes(bits, k):
 
 
 @pytest.mark.parametrize("m", [256, 255, 253, 251, 247, 241, 217, 173])
-def test_magic_reduction_exhaustive_epilogue_range(m):
-    """mod_small(s) = s - (umulhi(s, ceil(2^37/m)) >> 5) m for every s < 2^24
-    (the epilogue's range); sampled up to 2^27 (the packers')."""
-    magic = ((1 << 37) + m - 1) // m
-    assert magic < 1 << 32
+def test_magic_reduction_exhaustive(m):
+    """mod_small(s) = umulhi(s, ceil(2^32/m)) * (-m) + s (mod 2^32) for every
+    s < 2^24 (the epilogue's T_hi c16 + T_lo range; the packers' dp4a sums
+    stay below 2^19)."""
+    magic = ((1 << 32) + m - 1) // m
+    assert magic < 1 << 32 or m == 1
     s = np.arange(0, 1 << 24, dtype=np.uint64)
-    q = ((s * np.uint64(magic)) >> np.uint64(32)) >> np.uint64(5)
-    assert np.array_equal(s - q * np.uint64(m), s % np.uint64(m))
-    s = np.random.default_rng(m).integers(0, 1 << 27, size=1 << 20, dtype=np.uint64)
-    s = np.concatenate([s, np.arange((1 << 27) - 4096, 1 << 27, dtype=np.uint64)])
-    q = ((s * np.uint64(magic)) >> np.uint64(32)) >> np.uint64(5)
-    assert np.array_equal(s - q * np.uint64(m), s % np.uint64(m))
+    q = (s * np.uint64(magic)) >> np.uint64(32)
+    r = (q * np.uint64((1 << 32) - m) + s) & np.uint64(0xFFFFFFFF)
+    assert np.array_equal(r, s % np.uint64(m))
 
 
 def test_packer_residue_split():
