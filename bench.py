@@ -234,6 +234,7 @@ def main():
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
     launches = [0]
+    per_launch = {}
 
     def step(engine, record=None):
         fl = eng_flags[engine] | (0 if record is not None else F.ASYNC)
@@ -242,22 +243,26 @@ def main():
             if world == 1:
                 F.mw_product_device(A[b], B[b], Cbuf, p, u, v, lam, stream=stream, flags=fl,
                                     timing=tm if record is not None else None)
-                launches[0] += 3
+                launches[0] += per_launch.get(b, 0)
             else:
                 r0, rn = rows[b]
                 D.mw_product_device(A[b][:rn], B.get(b), Crow[:rn], p, u, v, lam, m, root=0,
                                     C_full=Cbuf, stream=stream, flags=fl,
                                     timing=tm if record is not None else None)
-                launches[0] += (2 if rn else 0) + (1 if rank == 0 else 0)
+                launches[0] += per_launch.get(b, 0)
             if record is not None:
-                record[b] = (tm.gemm_ms, tm.engine, tm.words)
+                record[b] = (tm.gemm_ms, tm.engine, tm.words, tm.launches)
 
     def barrier():
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
+    # first warm-up step recorded: each product's kernel-launch count (tm.launches)
+    rec0 = {}
+    step(args.engine, record=rec0)
+    per_launch.update({b: r[3] for b, r in rec0.items()})
+    for _ in range(args.warmup - 1):
         step(args.engine)
     barrier()
     launches[0] = 0
@@ -305,7 +310,7 @@ def main():
         work = gemm_total = 0.0
         ran = set()
         for (b, p, u, v, lam, lk) in probs:
-            g, e_ran, words = rec[b]
+            g, e_ran, words, _ = rec[b]
             ran.add(e_ran)
             rn = rows[b][1]
             if e_ran == F.ENGINE_DMMA:

@@ -120,8 +120,8 @@ int fpmm_b200_finish_plan(fpmm_b200_plan* plan, int64_t m, int64_t k, int64_t n)
 int fpmm_b200_kernel_block(uint64_t p, int u, int v, int64_t* lambda_k);
 /* RNS engine words: the smallest count n of the fixed pairwise-coprime byte
  * moduli (256, 255, 253, 251, ...) whose product M covers the centred exact
- * sum, 1000 M >= 2002 K floor(p/2)^2, and the CRT constants the fused
- * epilogue uses: y_i = (M/m_i)^-1 mod m_i, g_i = round(2^24 y_i / m_i),
+ * sum, 1000 M >= 2030 K floor(p/2)^2, and the CRT constants:
+ * y_i = (M/m_i)^-1 mod m_i, g_i = round(2^24 y_i / m_i),
  * W_i = y_i (M/m_i) mod p, Mp = M mod p.  Arrays hold FPMM_B200_RNS_MAX_MODULI. */
 #define FPMM_B200_RNS_MAX_MODULI 20
 int fpmm_b200_rns_plan(uint64_t p, int64_t k, int* nmod, uint32_t* moduli, uint32_t* y, uint32_t* g,

@@ -170,6 +170,7 @@ struct Job {
   int nmod = 0;  // RNS engine: moduli count
   rns::Params rp{};
   rns::PackParams rpp{};
+  rns::CrtParams rcp{};
 };
 
 template <typename F>
@@ -217,7 +218,7 @@ int auto_engine(i64 m, i64 k, i64 n, u64 p) {
   const double n_i8 = static_cast<double>((n + nt - 1) / nt * nt);
   const double n_rns = static_cast<double>((n + 255) / 256 * 256), m_rns = static_cast<double>((m + 255) / 256 * 256);
   const double t_i8 = D * D * 2.0 * m * k * n_i8 / 3.2e15 + (8.0 + D) * mk_kn / 4.5e12;
-  const double t_rns = nmod * 2.0 * m_rns * k * n_rns / 3.2e15 + (8.0 + nmod) * mk_kn / 3.0e12;
+  const double t_rns = nmod * 2.0 * m_rns * k * n_rns / 3.2e15 + (8.0 + nmod) * mk_kn / 4.5e12;
   return t_rns < t_i8 ? kRns : kI8;
 }
 
@@ -284,6 +285,22 @@ Job make_rns_job(i64 m, i64 k, i64 n, u64 p) {
   q.two32_sh = shoup(q.two32, p);
   q.Mp = pl.Mp;
   q.Mp_sh = shoup(pl.Mp, p);
+  rns::CrtParams& cp = j.rcp;
+  cp.nmod = j.nmod;
+  cp.p = p;
+  cp.mu = q.mu;
+  cp.two32 = q.two32;
+  cp.two32_sh = q.two32_sh;
+  cp.Mp = pl.Mp;
+  cp.Mp_sh = q.Mp_sh;
+  for (int i = 0; i < j.nmod; ++i) {
+    cp.mod[i] = pl.mod[i];
+    const u64 g = ((static_cast<u64>(pl.y[i]) << 19) + pl.mod[i] / 2) / pl.mod[i];  // < 2^19
+    for (int b = 0; b < rns::kCrtPlanes; ++b) {
+      const u64 byte = b < 7 ? (pl.W[i] >> (8 * b)) & 0xFF : (g >> (8 * (b - 7))) & 0xFF;
+      cp.wb[i / 4][b] |= static_cast<uint32_t>(byte) << (8 * (i % 4));
+    }
+  }
   rns::PackParams& pp = j.rpp;
   pp.half_p = static_cast<double>(p / 2);
   pp.nmod = j.nmod;
@@ -424,8 +441,8 @@ void launch_pack_b(const Job& j, const double* B, i64 ldb, void* bpack, int* err
   CUDA_OK(cudaGetLastError());
 }
 
-void launch_gemm_i8(const Job& j, const void* apack, const void* bpack, double* C, i64 ldc, i64 rows,
-                    cudaStream_t s) {
+int launch_gemm_i8(const Job& j, const void* apack, const void* bpack, double* C, i64 ldc, i64 rows,
+                   cudaStream_t s) {
   i8::Params q = j.ip;
   q.apack = static_cast<const uint8_t*>(apack);
   q.bpack = static_cast<const uint8_t*>(bpack);
@@ -484,6 +501,7 @@ void launch_gemm_i8(const Job& j, const void* apack, const void* bpack, double* 
                                                                         j.n, j.p);
     CUDA_OK(cudaGetLastError());
   }
+  return splits > 1 ? 2 : 1;
 }
 
 // 2-D uint8 tensor map over `bytes` of a packed operand viewed as 128-byte
@@ -511,24 +529,21 @@ CUtensorMap chunk_map(const void* base, size_t bytes) {
   return m;
 }
 
-void launch_gemm_rns(const Job& j, const void* apack, const void* bpack, double* C, i64 ldc, i64 rows,
-                     cudaStream_t s) {
+int launch_gemm_rns(const Job& j, const void* apack, const void* bpack, double* C, i64 ldc, i64 rows,
+                    cudaStream_t s) {
   rns::Params q = j.rp;
   q.apack = static_cast<const uint8_t*>(apack);
   q.bpack = static_cast<const uint8_t*>(bpack);
   q.tmA = chunk_map(apack, static_cast<size_t>((rows + rns::kPairM - 1) / rns::kPairM) * j.per_rb_bytes);
   q.tmB = chunk_map(bpack, j.bpack_bytes);
-  if (const char* d = std::getenv("FPMM_B200_RNS_DEBUG")) q.dbg = std::atoi(d);
-  q.group = rns::kGroup;
-  if (const char* d = std::getenv("FPMM_B200_RNS_GROUP")) q.group = std::max(1, std::atoi(d));
   q.C = C;
   q.ldc = ldc;
   q.m = rows;
   q.MB = static_cast<int>((rows + rns::kPairM - 1) / rns::kPairM);
-  // split-K when the output has too few pair tiles for the SM pairs (each slice runs
-  // its own CRT; partial residues are combined mod p), and one slice per
-  // exact int32 segment for long K (split-major: each wave streams one
-  // K-chunk of its panels)
+  // split-K when the output has too few pair tiles for the SM pairs, and one
+  // slice per exact int32 segment for long K (split-major: each wave streams
+  // one K-chunk of its panels); the slices' residues are summed mod m_i by
+  // the CRT kernel, which covers the full K (n_mod is planned for it)
   const i64 tiles0 = static_cast<i64>(q.MB) * q.NB;
   int splits = 1;
   if (tiles0 > 0 && tiles0 < 74) {
@@ -542,22 +557,17 @@ void launch_gemm_rns(const Job& j, const void* apack, const void* bpack, double*
   int dev = 0;
   CUDA_OK(cudaGetDevice(&dev));
   DeviceCtx& dc = ctx(dev);
-  double* work = nullptr;
-  if (splits > 1) {
-    work = static_cast<double*>(dc.splitws.get(sizeof(double) * splits * rows * j.n));
-    q.C = work;
-    q.ldc = j.n;
-    q.split_stride = rows * j.n;
-  }
   int sms = 148;
   CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const i64 items = static_cast<i64>(q.MB) * q.NB * splits;
   if (items > 0x7fffffff) throw Failure(FPMM_B200_EERROR, "problem too large for one launch");
   // persistent CTA pairs (clusters of 2 on neighbouring SMs)
   const unsigned grid = 2 * static_cast<unsigned>(std::max<i64>(1, std::min<i64>(items, sms / 2)));
-  // residue bytes of every item (modulus-major order: a tile's CRT runs in
-  // the pass of its last modulus), n bytes per output element
+  // residue bytes of every item: n bytes per output element and slice
   q.scratch = static_cast<uint8_t*>(dc.scratch.get(static_cast<size_t>(items) * 2 * j.nmod * rns::kSlotPerMod));
+  if (const char* d = std::getenv("FPMM_B200_RNS_DEBUG")) q.dbg = std::atoi(d);
+  q.group = rns::kGroup;
+  if (const char* d = std::getenv("FPMM_B200_RNS_GROUP")) q.group = std::max(1, std::atoi(d));
   static bool configured[64] = {};
   if (!configured[dev & 63]) {
     CUDA_OK(cudaFuncSetAttribute(rns::rns_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, rns::kSmem));
@@ -565,15 +575,23 @@ void launch_gemm_rns(const Job& j, const void* apack, const void* bpack, double*
   }
   rns::rns_kernel<<<grid, rns::kThreads, rns::kSmem, s>>>(q);
   CUDA_OK(cudaGetLastError());
-  if (splits > 1) {
-    i8::splitk_reduce_kernel<<<grid_for(rows * j.n, 256), 256, 0, s>>>(work, rows * j.n, splits, C, ldc, rows,
-                                                                        j.n, j.p);
-    CUDA_OK(cudaGetLastError());
-  }
+  // CRT of every tile (slices summed mod m_i first) straight into C
+  rns::CrtParams cp = j.rcp;
+  cp.R = q.scratch;
+  cp.C = C;
+  cp.ldc = ldc;
+  cp.m = rows;
+  cp.n = j.n;
+  cp.MB = q.MB, cp.NB = q.NB, cp.splits = splits, cp.group = q.group;
+  const i64 tiles = static_cast<i64>(q.MB) * q.NB;
+  rns::rns_crt_kernel<<<static_cast<unsigned>(2 * tiles), 256, 0, s>>>(cp);
+  CUDA_OK(cudaGetLastError());
+  return 2;
 }
 
-void launch_gemm(const Job& j, const void* apack_v, const void* bpack_v, double* C, i64 ldc, i64 rows,
-                 cudaStream_t s) {
+// Launches the product kernel(s) for packed operands; returns the launch count.
+int launch_gemm(const Job& j, const void* apack_v, const void* bpack_v, double* C, i64 ldc, i64 rows,
+                cudaStream_t s) {
   if (j.engine == kRns) return launch_gemm_rns(j, apack_v, bpack_v, C, ldc, rows, s);
   if (j.engine == kI8) return launch_gemm_i8(j, apack_v, bpack_v, C, ldc, rows, s);
   const double* apack = static_cast<const double*>(apack_v);
@@ -600,6 +618,7 @@ void launch_gemm(const Job& j, const void* apack_v, const void* bpack_v, double*
     kern<<<static_cast<unsigned>(tiles), Cfg::kThreads, Cfg::kSmem, s>>>(g);
   });
   CUDA_OK(cudaGetLastError());
+  return 1;
 }
 
 float elapsed(cudaEvent_t a, cudaEvent_t b) {
@@ -669,7 +688,7 @@ void product_device(const ProductArgs& a, int device, void* stream, fpmm_b200_ti
   launch_pack_a(j, a.A, a.lda, a.m, apack, err, s);
   launch_pack_b(j, a.B, a.ldb, bpack, err, s);
   if (tm) CUDA_OK(cudaEventRecord(c.ev[1], s));
-  launch_gemm(j, apack, bpack, a.C, a.ldc, a.m, s);
+  const int gl = launch_gemm(j, apack, bpack, a.C, a.ldc, a.m, s);
   if (tm) CUDA_OK(cudaEventRecord(c.ev[2], s));
   if (err) check_err_flag(c, s);
   if (tm) {
@@ -679,7 +698,7 @@ void product_device(const ProductArgs& a, int device, void* stream, fpmm_b200_ti
     tm->total_ms = elapsed(c.ev[0], c.ev[2]);
     tm->lambda_k = j.lambda_k;
     tm->engine = engine_flag(j), tm->words = engine_words(j);
-    tm->launches = 3;
+    tm->launches = 2 + gl;
     tm->ngpus = 1;
   }
   if (!(a.flags & FPMM_B200_ASYNC)) CUDA_OK(cudaStreamSynchronize(s));
@@ -764,7 +783,7 @@ void product_prepared_device(const Prepared* h, const double* dB, i64 ldb, doubl
   if (tm) CUDA_OK(cudaEventRecord(c.ev[0], s));
   launch_pack_b(j, dB, ldb, bpack, err, s);
   if (tm) CUDA_OK(cudaEventRecord(c.ev[1], s));
-  launch_gemm(j, h->words.ptr, bpack, dC, ldc, h->m, s);
+  const int gl = launch_gemm(j, h->words.ptr, bpack, dC, ldc, h->m, s);
   if (tm) CUDA_OK(cudaEventRecord(c.ev[2], s));
   if (err) check_err_flag(c, s);
   if (tm) {
@@ -774,7 +793,7 @@ void product_prepared_device(const Prepared* h, const double* dB, i64 ldb, doubl
     tm->total_ms = elapsed(c.ev[0], c.ev[2]);
     tm->lambda_k = j.lambda_k;
     tm->engine = engine_flag(j), tm->words = engine_words(j);
-    tm->launches = 2;
+    tm->launches = 1 + gl;
     tm->ngpus = 1;
   }
   if (!(fl & FPMM_B200_ASYNC)) CUDA_OK(cudaStreamSynchronize(s));
@@ -862,12 +881,13 @@ void product_host(const ProductArgs& a, int ngpus, fpmm_b200_timing* tm) {
     CUDA_OK(cudaStreamWaitEvent(s, c.ev[1], 0));
     CUDA_OK(cudaEventRecord(c.ev[2], s));
     launch_pack_b(j, dB, a.n, bpack, err, s);
+    int nl = 1;
     for (int i = 0; i < nch; ++i) {
       const i64 r0 = i * chunk_rows, rn = std::min<i64>(a.m - r0, chunk_rows);
       uint8_t* ap = apack + static_cast<size_t>(r0 / j.BM) * per_rb;
       CUDA_OK(cudaStreamWaitEvent(s, c.ev_in[i], 0));
       launch_pack_a(j, dA + r0 * a.k, a.k, rn, ap, err, s);
-      launch_gemm(j, ap, bpack, dC + r0 * a.n, a.n, rn, s);
+      nl += 1 + launch_gemm(j, ap, bpack, dC + r0 * a.n, a.n, rn, s);
       CUDA_OK(cudaEventRecord(c.ev_out[i], s));
       CUDA_OK(cudaStreamWaitEvent(so, c.ev_out[i], 0));
       CUDA_OK(cudaMemcpy2DAsync(a.C + r0 * a.ldc, a.ldc * 8, dC + r0 * a.n, a.n * 8, a.n * 8, rn,
@@ -882,8 +902,8 @@ void product_host(const ProductArgs& a, int ngpus, fpmm_b200_timing* tm) {
       tm->d2h_ms = elapsed(c.ev_out[nch - 1], c.ev[3]);  // exposed tail of the D2H
       tm->total_ms = elapsed(c.ev[0], c.ev[3]);
       tm->lambda_k = j.lambda_k;
-    tm->engine = engine_flag(j), tm->words = engine_words(j);
-      tm->launches = 1 + 2 * nch;
+      tm->engine = engine_flag(j), tm->words = engine_words(j);
+      tm->launches = nl;
       tm->ngpus = 1;
     }
     return;
@@ -935,11 +955,12 @@ void product_host(const ProductArgs& a, int ngpus, fpmm_b200_timing* tm) {
     NCCL_OK(nccl().Broadcast(bpack[0], bpack[g], j.bpack_bytes, ncclUint8, 0, g_all.comms[g], cs[g]->stream));
   }
   NCCL_OK(nccl().GroupEnd());
+  int nl = 1;
   for (int g = 0; g < ngpus; ++g) {
     DeviceCtx& c = *cs[g];
     CUDA_OK(cudaSetDevice(g));
     CUDA_OK(cudaEventRecord(c.ev[3], c.stream));
-    if (rn[g] > 0) launch_gemm(j, apack[g], bpack[g], dC[g], a.n, rn[g], c.stream);
+    if (rn[g] > 0) nl += 1 + launch_gemm(j, apack[g], bpack[g], dC[g], a.n, rn[g], c.stream);
     CUDA_OK(cudaEventRecord(c.ev[4], c.stream));
     if (rn[g] > 0)
       CUDA_OK(cudaMemcpy2DAsync(a.C + r0[g] * a.ldc, a.ldc * 8, dC[g], a.n * 8, a.n * 8, rn[g],
@@ -964,7 +985,7 @@ void product_host(const ProductArgs& a, int ngpus, fpmm_b200_timing* tm) {
     tm->total_ms = total;
     tm->lambda_k = j.lambda_k;
     tm->engine = engine_flag(j), tm->words = engine_words(j);
-    tm->launches = 2 * ngpus + 1;
+    tm->launches = nl;
     tm->ngpus = ngpus;
   }
 }
@@ -1250,9 +1271,9 @@ void dist_product_device(const double* dA_rows, i64 lda, const double* dB, i64 l
   CUDA_OK(cudaEventRecord(c.ev[1], s));
   NCCL_OK(nccl().Broadcast(bpack, bpack, j.bpack_bytes, ncclUint8, root, g_dist.comm, s));
   CUDA_OK(cudaEventRecord(c.ev[2], s));
-  if (rn > 0) launch_gemm(j, apack, bpack, dC_rows, ldc, rn, s);
+  const int gl = rn > 0 ? launch_gemm(j, apack, bpack, dC_rows, ldc, rn, s) : 0;
   CUDA_OK(cudaEventRecord(c.ev[3], s));
-  int launches = (rn > 0 ? 2 : 0) + (g_dist.rank == root ? 1 : 0);
+  int launches = (rn > 0 ? 1 + gl : 0) + (g_dist.rank == root ? 1 : 0);
   if (dC_full) {
     // gather row blocks to root (grouped point-to-point; NCCL has no gather)
     if (ldc != n || (g_dist.rank == root && ldc_full != n))

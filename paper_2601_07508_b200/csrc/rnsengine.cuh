@@ -54,7 +54,7 @@ constexpr int kThreads = 320;        // 10 warps
 constexpr int kEpiWarps = 8;
 constexpr int kSmem = kStages * kStageBytes + 1024;
 constexpr int kSlotPerMod = kBM * kNT;  // scratch bytes per modulus per CTA tile (32 KB)
-constexpr int kGroup = 6;               // pair-tile rows per rasterisation group
+constexpr int kGroup = 16;              // pair-tile rows per rasterisation group
 
 // Per-modulus constants (host: rns_plan in rules.cpp).
 struct Params {
@@ -241,7 +241,7 @@ __device__ __forceinline__ uint4* scratch_at(uint8_t* slot, int i, int half, int
 
 // Reduce 32 TMEM columns (one tcgen05.ld) mod m and park them as 2 x 16 bytes.
 __device__ __forceinline__ void park32(const uint32_t (&v)[32], uint32_t m, uint32_t negm, uint32_t c16, uint32_t magic,
-                                       bool acc, uint4* dst0, uint4* dst1) {
+                                       bool acc, bool stream, uint4* dst0, uint4* dst1) {
   uint32_t w[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
@@ -269,52 +269,155 @@ __device__ __forceinline__ void park32(const uint32_t (&v)[32], uint32_t m, uint
       w[q] = word;
     }
   }
-  *dst0 = make_uint4(w[0], w[1], w[2], w[3]);
-  *dst1 = make_uint4(w[4], w[5], w[6], w[7]);
+  if (stream) {  // read back only by the CRT kernel: keep them from evicting operand panels
+    __stcs(dst0, make_uint4(w[0], w[1], w[2], w[3]));
+    __stcs(dst1, make_uint4(w[4], w[5], w[6], w[7]));
+  } else {
+    *dst0 = make_uint4(w[0], w[1], w[2], w[3]);
+    *dst1 = make_uint4(w[4], w[5], w[6], w[7]);
+  }
 }
 
-// CRT of 8 columns (half `sub` of a 16-byte residue row) of one row -> C.
-// All nmod residue words are loaded before any is used, so the parked bytes
-// (possibly evicted to HBM by the time the tile ends) cost one round trip.
-__device__ __forceinline__ void crt8(const Params& P, uint8_t* slot, int half, int c16, int sub, int row_in_tile,
-                                     i64 row, i64 col0, double* dst) {
-  uint2 rw[kMaxMod];
+// ------------------------------------------------------------------ CRT
+// C = X mod p from the parked residue bytes of every tile (summed over the
+// split-K slices mod m_i first: residues are additive):
+//   X mod p = (sum r_i W_i - t (M mod p)) mod p,  t = round(sum r_i y_i / m_i),
+// W_i = y_i M_i mod p (7 bytes), g_i = round(2^19 y_i / m_i) (3 bytes).  Both
+// sums are evaluated byte-plane by byte-plane with dp4a over groups of four
+// moduli: the residue words of four moduli are transposed (PRMT) so one word
+// holds one element's four residues, and plane b accumulates
+// sum_i r_i byte_b(W_i) (< 20 * 255^2 < 2^21).  That is 10 dp4a per element
+// per four moduli.  The fixed-point error of t is <= n 255 2^-20 <= 0.005,
+// inside the plan's range margin (|X| / M <= 1/2.03).
+constexpr int kCrtPlanes = 10;                 // 7 byte planes of W, 3 of g
+constexpr int kCrtGroups = (kMaxMod + 3) / 4;  // groups of four moduli
+struct CrtParams {
+  const uint8_t* R;  // residue blocks, as parked by rns_kernel
+  double* C;
+  i64 ldc, m, n;
+  int MB, NB, nmod, splits, group;
+  unsigned long long p, mu, two32, two32_sh, Mp, Mp_sh;
+  uint32_t mod[kMaxMod];
+  uint32_t wb[kCrtGroups][kCrtPlanes];  // byte b of W_i (b < 7) / g_i (b >= 7) for the group's 4 moduli
+};
+
+// CRT of one thread's 128 columns, four per step.  All n residue words of a
+// step are loaded before any is used (n independent loads in flight per
+// thread); SPLIT: the slices' residues are summed first.
+template <bool SPLIT>
+__device__ __forceinline__ void crt_row(const CrtParams& P, const uint8_t* __restrict__ pthr, i64 slice_stride,
+                                        i64 colh, double* __restrict__ dst_row) {
+  const unsigned long long p = P.p;
+  const int ngroups = (P.nmod + 3) / 4;
+#pragma unroll 1
+  for (int c = 0; c < (kNT / 2) / 4; ++c) {
+    const i64 col0 = colh + c * 4;
+    if (col0 >= P.n) break;
+    const uint8_t* pc = pthr + (c >> 2) * (16 * kBM) + (c & 3) * 4;
+    uint32_t rw[kMaxMod];
 #pragma unroll
-  for (int i = 0; i < kMaxMod; ++i)
-    if (i < P.nmod) rw[i] = reinterpret_cast<const uint2*>(scratch_at(slot, i, half, c16, row_in_tile))[sub];
-  if (row >= P.m) return;
-  unsigned long long s_lo[8], s_hi[8], f[8];
+    for (int i = 0; i < kMaxMod; ++i) {
+      if (i >= P.nmod) {
+        rw[i] = 0;
+      } else if (!SPLIT) {
+        rw[i] = __ldg(reinterpret_cast<const uint32_t*>(pc + i * kSlotPerMod));
+      } else {
+        uint32_t r = *reinterpret_cast<const uint32_t*>(pc + i * kSlotPerMod);
+        for (int s = 1; s < P.splits; ++s) {  // add the other slices' residues mod m_i
+          const uint32_t o = *reinterpret_cast<const uint32_t*>(pc + s * slice_stride + i * kSlotPerMod);
+          uint32_t out = 0;
 #pragma unroll
-  for (int e = 0; e < 8; ++e) s_lo[e] = s_hi[e] = f[e] = 0;
+          for (int e = 0; e < 4; ++e) {
+            uint32_t v = ((r >> (8 * e)) & 0xFFu) + ((o >> (8 * e)) & 0xFFu);
+            v = v >= P.mod[i] ? v - P.mod[i] : v;
+            out |= v << (8 * e);
+          }
+          r = out;
+        }
+        rw[i] = r;
+      }
+    }
+    uint32_t acc[4][kCrtPlanes];
 #pragma unroll
-  for (int i = 0; i < kMaxMod; ++i) {
-    if (i >= P.nmod) break;
-    const uint32_t w2[2] = {rw[i].x, rw[i].y};
-    const uint32_t wl = P.w_lo[i], wh = P.w_hi[i], g = P.g[i];
+    for (int e = 0; e < 4; ++e)
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const uint32_t r = (w2[e / 4] >> (8 * (e % 4))) & 0xFFu;
-      s_lo[e] += static_cast<unsigned long long>(r) * wl;
-      s_hi[e] += static_cast<unsigned long long>(r) * wh;
-      f[e] += static_cast<unsigned long long>(r) * g;
+      for (int b = 0; b < kCrtPlanes; ++b) acc[e][b] = 0;
+#pragma unroll
+    for (int gi = 0; gi < kCrtGroups; ++gi) {
+      if (gi >= ngroups) break;
+      // transpose: t[e] = the four moduli's residues of column e
+      const uint32_t a0 = rw[4 * gi], a1 = rw[4 * gi + 1], a2 = rw[4 * gi + 2], a3 = rw[4 * gi + 3];
+      const uint32_t u0 = __byte_perm(a0, a1, 0x5140), u1 = __byte_perm(a0, a1, 0x7362);
+      const uint32_t u2 = __byte_perm(a2, a3, 0x5140), u3 = __byte_perm(a2, a3, 0x7362);
+      const uint32_t t[4] = {__byte_perm(u0, u2, 0x5410), __byte_perm(u0, u2, 0x7632), __byte_perm(u1, u3, 0x5410),
+                             __byte_perm(u1, u3, 0x7632)};
+#pragma unroll
+      for (int b = 0; b < kCrtPlanes; ++b) {
+        const uint32_t wb = P.wb[gi][b];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[e][b] = __dp4a(t[e], wb, acc[e][b]);
+      }
+    }
+    double out[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint32_t* a = acc[e];
+      // t = round(F / 2^19), F = a7 + 2^8 a8 + 2^16 a9: with u = a8 + 2^8 a9 + (a7 >> 8),
+      // F = 2^8 u + (a7 & 255) and t = (u + 2^10) >> 11 exactly (32-bit)
+      const uint32_t tt = (a[8] + (a[9] << 8) + (a[7] >> 8) + 1024u) >> 11;
+      // S = sum_i r_i W_i = sum_b 2^(8b) a_b (b < 7)
+      unsigned long long sm;
+      if (P.nmod <= 16) {  // S < 16 * 255 * 2^52 < 2^64: one u64 and one Barrett
+        const unsigned long long S = a[0] + (static_cast<unsigned long long>(a[1]) << 8) +
+                                     (static_cast<unsigned long long>(a[2]) << 16) +
+                                     (static_cast<unsigned long long>(a[3]) << 24) +
+                                     (static_cast<unsigned long long>(a[4]) << 32) +
+                                     (static_cast<unsigned long long>(a[5]) << 40) +
+                                     (static_cast<unsigned long long>(a[6]) << 48);
+        sm = barrett(S, p, P.mu);
+      } else {
+        const unsigned long long lo = a[0] + (static_cast<unsigned long long>(a[1]) << 8) +
+                                      (static_cast<unsigned long long>(a[2]) << 16) +
+                                      (static_cast<unsigned long long>(a[3]) << 24);  // < 2^45
+        const unsigned long long hi = a[4] + (static_cast<unsigned long long>(a[5]) << 8) +
+                                      (static_cast<unsigned long long>(a[6]) << 16);  // < 2^37
+        sm = barrett(dev::shoup_mulmod(hi, P.two32, P.two32_sh, p) + lo, p, P.mu);
+      }
+      // t M mod p: for n <= 16, t < 2^12 and t (M mod p) < 2^64 is one u64
+      const unsigned long long tmod = P.nmod <= 16 ? barrett(static_cast<unsigned long long>(tt) * P.Mp, p, P.mu)
+                                                   : dev::shoup_mulmod(tt, P.Mp, P.Mp_sh, p);
+      const unsigned long long r = sm >= tmod ? sm - tmod : sm + p - tmod;
+      out[e] = __longlong_as_double(static_cast<long long>(r | 0x4330000000000000ull)) - 4503599627370496.0;
+    }
+    double* dst = dst_row + c * 4;
+    if (col0 + 4 <= P.n && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+      *reinterpret_cast<double2*>(dst) = make_double2(out[0], out[1]);
+      *reinterpret_cast<double2*>(dst + 2) = make_double2(out[2], out[3]);
+    } else {
+      for (int e = 0; e < 4 && col0 + e < P.n; ++e) dst[e] = out[e];
     }
   }
-  const unsigned long long p = P.p;
-  double out[8];
-#pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    const unsigned long long t = (f[e] + (1ull << 23)) >> 24;  // round(Z / M)
-    const unsigned long long hi = dev::shoup_mulmod(s_hi[e], P.two32, P.two32_sh, p);
-    const unsigned long long s = barrett(hi + s_lo[e], p, P.mu);
-    const unsigned long long tm = dev::shoup_mulmod(t, P.Mp, P.Mp_sh, p);
-    out[e] = static_cast<double>(s >= tm ? s - tm : s + p - tm);
-  }
-  if (col0 + 8 <= P.n && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-#pragma unroll
-    for (int e = 0; e < 8; e += 2) *reinterpret_cast<double2*>(dst + e) = make_double2(out[e], out[e + 1]);
-  } else {
-    for (int e = 0; e < 8 && col0 + e < P.n; ++e) dst[e] = out[e];
-  }
+}
+
+// One block of 256 threads per (pair tile, CTA rank): thread = (column half, row).
+__global__ void __launch_bounds__(256) rns_crt_kernel(const __grid_constant__ CrtParams P) {
+  const int tile = blockIdx.x >> 1, rank = blockIdx.x & 1;
+  const int row_in_tile = threadIdx.x % kBM, half = threadIdx.x / kBM;
+  Params q{};
+  q.MB = P.MB, q.NB = P.NB, q.splits = P.splits, q.group = P.group;
+  const Item it = item_of(tile, q);  // the tile of items t = tile + s * tiles (s = split)
+  const i64 row = (2 * static_cast<i64>(it.tm) + rank) * kBM + row_in_tile;
+  if (row >= P.m) return;
+  const i64 colh = static_cast<i64>(it.tn) * kNT + half * (kNT / 2);
+  const i64 tiles = static_cast<i64>(P.MB) * P.NB;
+  // this thread's bytes in the tile's residue block: modulus i, 8-column step c at
+  // i * kSlotPerMod + (c / 2) * 16 kBM + (c % 2) * 8 (see scratch_at)
+  const uint8_t* pthr = P.R + (static_cast<i64>(tile) * 2 + rank) * P.nmod * kSlotPerMod +
+                        (static_cast<i64>(half) * 8 * kBM + row_in_tile) * 16;
+  const i64 slice_stride = tiles * 2 * P.nmod * kSlotPerMod;
+  double* dst_row = P.C + row * P.ldc + colh;
+  if (P.splits == 1) crt_row<false>(P, pthr, slice_stride, colh, dst_row);
+  else crt_row<true>(P, pthr, slice_stride, colh, dst_row);
 }
 
 // ---- CTA-pair plumbing ----
@@ -442,7 +545,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
     // complete on it, so the leader's one wait covers the pair.
     if (lane == 0) {
       // (evict_last for A / evict_first for B measured 2-10% slower than normal)
-      const uint64_t polA = policy_evict_normal(), polB = polA;
+      const uint64_t polA = (P.dbg & 128) ? policy_evict_last() : policy_evict_normal();
+      const uint64_t polB = (P.dbg & 128) ? policy_evict_first() : policy_evict_normal();
       int g = 0;
       for (int i = 0; i < P.nmod; ++i) {
         for (int t = pair; t < total; t += npairs) {
@@ -537,19 +641,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
               if (lane == 0) mbar_arrive_cluster(leader_tmem_empty + b * 8);
             }
             if (!(P.dbg & 10))
-              park32(v, m, nm, c16, mg, seg > 0, scratch_at(slot, i, half, c0 / 16, row_in_tile),
+              park32(v, m, nm, c16, mg, seg > 0, !(P.dbg & 32), scratch_at(slot, i, half, c0 / 16, row_in_tile),
                      scratch_at(slot, i, half, c0 / 16 + 1, row_in_tile));
-          }
-        }
-        if (i + 1 == P.nmod && !(P.dbg & 6)) {
-          // CRT over the tile's parked residues of this thread's row / column half
-          const i64 row = (2 * static_cast<i64>(it.tm) + rank) * kBM + row_in_tile;
-          const i64 colh = static_cast<i64>(it.tn) * kNT + half * (kNT / 2);
-          double* dst_row = P.C + static_cast<i64>(it.ks) * P.split_stride + row * P.ldc + colh;
-#pragma unroll 1
-          for (int c = 0; c < (kNT / 2) / 8; ++c) {
-            if (colh + c * 8 >= P.n) break;
-            crt8(P, slot, half, c / 2, c % 2, row_in_tile, row, colh + c * 8, dst_row + c * 8);
           }
         }
       }

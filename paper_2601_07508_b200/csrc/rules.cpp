@@ -276,8 +276,8 @@ const std::uint32_t* rns_moduli_list() { return kRnsModuli; }
 RnsPlan rns_plan(u64 p, i64 k) {
   if (p < 2) throw Failure(FPMM_B200_EERROR, "rns_plan: p must exceed 1");
   const u64 h = p / 2, kk = static_cast<u64>(std::max<i64>(k, 1));
-  Big need{1};  // 2002 K h^2
-  big_mul(need, 2002);
+  Big need{1};  // 2030 K h^2
+  big_mul(need, 2030);
   big_mul(need, kk);
   big_mul(need, h);
   big_mul(need, h);

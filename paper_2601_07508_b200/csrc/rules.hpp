@@ -87,16 +87,16 @@ namespace fpmm_b200 {
 //
 // Centred residues x' = x - p [x > p/2] are represented modulo n pairwise
 // coprime moduli m_i <= 256 (one byte each).  n is the smallest count with
-// 1000 M >= 2002 K floor(p/2)^2 (M = prod m_i), so the exact integer
-// X = sum_k a'_k b'_k (|X| <= K floor(p/2)^2) is recovered by the CRT with
-// the rounding of t = round(sum r_i y_i / m_i) (fixed point 2^-24, error
-// <= n 2^-17) kept clear of the +-1/2 boundary.
+// 1000 M >= 2030 K floor(p/2)^2 (M = prod m_i), so the exact integer
+// X = sum_k a'_k b'_k (|X| <= K floor(p/2)^2, |X| / M <= 1/2.03) is recovered
+// by the CRT with the rounding of t = round(sum r_i y_i / m_i) (fixed point
+// 2^-19, error <= n 255 2^-20 <= 0.005) kept clear of the +-1/2 boundary.
 constexpr int kRnsMaxMod = 20;
 struct RnsPlan {
   int n = 0;
   std::uint32_t mod[kRnsMaxMod] = {};
   std::uint32_t y[kRnsMaxMod] = {};       // (M/m_i)^{-1} mod m_i
-  std::uint32_t g[kRnsMaxMod] = {};       // round(2^24 y_i / m_i)
+  std::uint32_t g[kRnsMaxMod] = {};       // round(2^24 y_i / m_i) (the C-ABI's exported scale)
   u64 W[kRnsMaxMod] = {};                 // y_i (M/m_i) mod p
   u64 Mp = 0;                             // M mod p
   double log2M = 0, log2X = 0;            // log2 M and log2(2 K floor(p/2)^2)

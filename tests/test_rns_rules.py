@@ -33,8 +33,8 @@ def test_modulus_count_is_minimal_and_covers_the_range(bits, k):
     pl = F.rns_plan(p, k)
     mods = pl["moduli"]
     h = p // 2
-    assert 1000 * prod(mods) >= 2002 * k * h * h
-    assert 1000 * prod(mods[:-1]) < 2002 * k * h * h or len(mods) == 1
+    assert 1000 * prod(mods) >= 2030 * k * h * h
+    assert 1000 * prod(mods[:-1]) < 2030 * k * h * h or len(mods) == 1
     for i in range(len(mods)):
         for j in range(i):
             assert math.gcd(mods[i], mods[j]) == 1
@@ -81,24 +81,39 @@ def barrett(x, p):
 
 
 def device_crt(X, p, pl):
-    """crt8() of rnsengine.cuh on the residues of X, in the kernel's u64 arithmetic."""
-    s_lo = s_hi = f = 0
-    for m, g, W in zip(pl["moduli"], pl["g"], pl["W"]):
+    """rns_crt_kernel() on the residues of X: byte-plane dp4a sums over groups
+    of four moduli, then the u64 Shoup / Barrett reconstruction."""
+    planes = [0] * 10
+    for m, y, W in zip(pl["moduli"], pl["y"], pl["W"]):
         r = X % m
-        s_lo += r * (W & 0xFFFFFFFF)
-        s_hi += r * (W >> 32)
-        f += r * g
-    assert s_lo < 1 << 64 and s_hi < 1 << 64 and f < 1 << 64
-    t = (f + (1 << 23)) >> 24
-    two32 = (1 << 32) % p
-    hi = shoup_mulmod(s_hi, two32, shoup(two32, p), p)
-    s = barrett(hi + s_lo, p)
-    tm = shoup_mulmod(t, pl["Mp"], shoup(pl["Mp"], p), p)
+        g = ((y << 19) + m // 2) // m
+        assert g < 1 << 19 and W < 1 << 56
+        for b in range(10):
+            wb = (W >> (8 * b)) & 0xFF if b < 7 else (g >> (8 * (b - 7))) & 0xFF
+            planes[b] += r * wb
+    assert max(planes) < 1 << 32  # 32-bit dp4a accumulators
+    t = (planes[8] + (planes[9] << 8) + (planes[7] >> 8) + 1024) >> 11
+    f = planes[7] + (planes[8] << 8) + (planes[9] << 16)
+    assert t == (f + (1 << 18)) >> 19  # the kernel's 32-bit rounding == round(F / 2^19)
+    if len(pl["moduli"]) <= 16:
+        S = sum(planes[b] << (8 * b) for b in range(7))
+        assert S < 1 << 64
+        s = barrett(S, p)
+    else:
+        lo = sum(planes[b] << (8 * b) for b in range(4))
+        hi = sum(planes[4 + b] << (8 * b) for b in range(3))
+        two32 = (1 << 32) % p
+        s = barrett(shoup_mulmod(hi, two32, shoup(two32, p), p) + lo, p)
+    if len(pl["moduli"]) <= 16:
+        assert t * pl["Mp"] < 1 << 64
+        tm = barrett(t * pl["Mp"], p)
+    else:
+        tm = shoup_mulmod(t, pl["Mp"], shoup(pl["Mp"], p), p)
     return s - tm if s >= tm else s + p - tm
 
 
 @pytest.mark.parametrize("bits", [3, 8, 20, 25, 33, 40, 48, 52])
-@pytest.mark.parametrize("k", [1, 100, 8192, 66048])
+@pytest.mark.parametrize("k", [1, 100, 8192, 66048, 1 << 20, 1 << 26])
 def test_device_crt_reconstruction_at_the_range_extremes(bits, k):
     p = F.prev_prime(1 << bits)
     pl = F.rns_plan(p, k)
