@@ -124,6 +124,9 @@ int fpmm_b200_kernel_block(uint64_t p, int u, int v, int64_t* lambda_k);
  * y_i = (M/m_i)^-1 mod m_i, g_i = round(2^24 y_i / m_i),
  * W_i = y_i (M/m_i) mod p, Mp = M mod p.  Arrays hold FPMM_B200_RNS_MAX_MODULI. */
 #define FPMM_B200_RNS_MAX_MODULI 20
+/* The engine the library default (no ENGINE_* flag) runs for an m x k by k x n
+ * product mod p: FPMM_B200_ENGINE_I8 or FPMM_B200_ENGINE_RNS (B200 time model). */
+int fpmm_b200_select_engine(int64_t m, int64_t k, int64_t n, uint64_t p, unsigned* engine_flag);
 int fpmm_b200_rns_plan(uint64_t p, int64_t k, int* nmod, uint32_t* moduli, uint32_t* y, uint32_t* g,
                        uint64_t* W, uint64_t* Mp);
 

@@ -25,7 +25,7 @@ __all__ = [
     "FpContext", "WordDecomposition", "ProductPlan", "Variant", "kVariants", "Timing",
     "is_prime_u64", "prev_prime", "bitsize", "word_base", "word_bound", "max_block_size",
     "mw_block_size", "variant_bit_limit", "variant_admits_bits", "select_variant",
-    "plan_for_modulus", "finish_plan", "kernel_block", "rns_plan", "mix_seed", "matrix_seed", "random_mat",
+    "plan_for_modulus", "finish_plan", "kernel_block", "rns_plan", "select_engine", "mix_seed", "matrix_seed", "random_mat",
     "decompose", "mw_product", "mw_product_words", "mw_product_workspace",
     "mw_product_workspace_words", "mw_product_concat", "mw_product_concat_words",
     "block_gemm_mod", "GemmKernel", "kernel_by_name", "b200_kernel", "mw_product_device",
@@ -139,6 +139,7 @@ def lib():
         "fpmm_b200_finish_plan": (i32, [C.POINTER(_Plan), i64, i64, i64]),
         "fpmm_b200_kernel_block": (i32, [u64, i32, i32, _i64p]),
         "fpmm_b200_rns_plan": (i32, [u64, i64, C.POINTER(i32), vp, vp, vp, vp, _u64p]),
+        "fpmm_b200_select_engine": (i32, [i64, i64, i64, u64, C.POINTER(C.c_uint)]),
         "fpmm_b200_mix_seed": (u64, [u64, u64]),
         "fpmm_b200_matrix_seed": (u64, [u64, i32, i64, i64, i64, u64]),
         "fpmm_b200_random_mat": (i32, [i64, i64, u64, u64, _dp]),
@@ -373,6 +374,13 @@ def rns_plan(p: int, k: int) -> dict:
     c = n.value
     return {"n": c, "moduli": list(mods[:c]), "y": list(y[:c]), "g": list(g[:c]), "W": list(W[:c]),
             "Mp": Mp.value}
+
+
+def select_engine(m: int, k: int, n: int, p: int) -> str:
+    """The engine the library default runs for this product shape: "i8" or "rns"."""
+    out = C.c_uint()
+    _check(lib().fpmm_b200_select_engine(m, k, n, p, C.byref(out)))
+    return "rns" if out.value == ENGINE_RNS else "i8"
 
 
 # ------------------------------------------------------------ synthetic inputs

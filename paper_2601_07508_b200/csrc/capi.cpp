@@ -135,6 +135,10 @@ int fpmm_b200_rns_plan(uint64_t p, int64_t k, int* nmod, uint32_t* moduli, uint3
   });
 }
 
+int fpmm_b200_select_engine(int64_t m, int64_t k, int64_t n, uint64_t p, unsigned* engine_flag) {
+  return guarded([&] { *engine_flag = select_engine(m, k, n, p); });
+}
+
 // mat.hpp:104-110 (splitmix64 step)
 uint64_t fpmm_b200_mix_seed(uint64_t a, uint64_t b) {
   uint64_t z = a + 0x9e3779b97f4a7c15ull * (b + 1);

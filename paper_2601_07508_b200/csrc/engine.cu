@@ -200,10 +200,11 @@ int resolve_engine(unsigned flags) {
 }
 
 // The library default between the two tcgen05 engines, by a time model fitted
-// on B200 (8192^3 sweep, profiles/round1/bench_sweep8192.json): the base-256
-// engine costs D^2 int8 GEMMs on NT-column tiles, the RNS engine n_mod GEMMs
-// on 256 x 256 pair tiles (about the same time each) and packs n_mod instead
-// of D bytes per element.
+// on B200 (profiles/round1: the 8192^3 sweep and configs.json): the base-256
+// engine costs D^2 int8 GEMMs on NT-column tiles plus a (2D-1)-block epilogue
+// per output element; the RNS engine n_mod GEMMs on 256 x 256 pair tiles plus
+// per-element residue parking and CRT; both pack their words (D or n_mod bytes
+// per element) and lose the idle SMs when there are too few (split) tiles.
 int auto_engine(i64 m, i64 k, i64 n, u64 p) {
   const int D = std::max(1, (bitsize(p - 1) + 7) / 8);
   int nmod = 0;
@@ -214,11 +215,23 @@ int auto_engine(i64 m, i64 k, i64 n, u64 p) {
   }
   int nt = 32;
   dispatch_d(D, [&]<int DD>() { nt = i8::Cfg<DD>::kNT; });
+  const i64 KB = (k + 63) / 64;
+  // fraction of the SMs (pairs) a product keeps busy, split-K included
+  auto busy = [&](i64 tiles, i64 slots) {
+    i64 items = tiles;
+    if (tiles < slots) items = tiles * std::max<i64>(1, std::min<i64>({(slots + tiles - 1) / tiles, KB / 16, 32}));
+    return std::min(1.0, static_cast<double>(items) / static_cast<double>(slots));
+  };
+  const double mn = static_cast<double>(m) * n;
   const double mk_kn = static_cast<double>(m) * k + static_cast<double>(k) * n;
   const double n_i8 = static_cast<double>((n + nt - 1) / nt * nt);
   const double n_rns = static_cast<double>((n + 255) / 256 * 256), m_rns = static_cast<double>((m + 255) / 256 * 256);
-  const double t_i8 = D * D * 2.0 * m * k * n_i8 / 3.2e15 + (8.0 + D) * mk_kn / 4.5e12;
-  const double t_rns = nmod * 2.0 * m_rns * k * n_rns / 3.2e15 + (8.0 + nmod) * mk_kn / 4.5e12;
+  const double t_i8 = (D * D * 2.0 * m * k * n_i8 / 3.2e15 + (2 * D - 1) * mn * 1.8e-12) /
+                          busy(((m + 127) / 128) * ((n + nt - 1) / nt), 148) +
+                      (8.0 + D) * mk_kn / 4.5e12;
+  const double t_rns = (nmod * 2.0 * m_rns * k * n_rns / 3.2e15 + nmod * mn * 0.95e-12) /
+                           busy(((m + 255) / 256) * ((n + 255) / 256), 74) +
+                       (8.0 + nmod) * mk_kn / 4.5e12;
   return t_rns < t_i8 ? kRns : kI8;
 }
 
@@ -568,6 +581,8 @@ int launch_gemm_rns(const Job& j, const void* apack, const void* bpack, double* 
   if (const char* d = std::getenv("FPMM_B200_RNS_DEBUG")) q.dbg = std::atoi(d);
   q.group = rns::kGroup;
   if (const char* d = std::getenv("FPMM_B200_RNS_GROUP")) q.group = std::max(1, std::atoi(d));
+  q.prefetch = 0;
+  if (const char* d = std::getenv("FPMM_B200_RNS_PREFETCH")) q.prefetch = std::max(0, std::atoi(d));
   static bool configured[64] = {};
   if (!configured[dev & 63]) {
     CUDA_OK(cudaFuncSetAttribute(rns::rns_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, rns::kSmem));
@@ -641,6 +656,13 @@ void zero_c(double* C, i64 ldc, i64 rows, i64 n, cudaStream_t s) {
 }
 
 }  // namespace
+
+unsigned select_engine(i64 m, i64 k, i64 n, u64 p) {
+  if (m < 0 || k < 0 || n < 0) throw Failure(FPMM_B200_EERROR, "matrix dimensions must be nonnegative");
+  if (p < 2) throw Failure(FPMM_B200_EERROR, "modulus must exceed 1");
+  return auto_engine(std::max<i64>(m, 1), std::max<i64>(k, 1), std::max<i64>(n, 1), p) == kRns ? FPMM_B200_ENGINE_RNS
+                                                                                             : FPMM_B200_ENGINE_I8;
+}
 
 void validate_product(u64 p, int u, int v, u64 lambda, i64 m, i64 k, i64 n, unsigned flags) {
   if (m < 0 || k < 0 || n < 0) throw Failure(FPMM_B200_EERROR, "matrix dimensions must be nonnegative");

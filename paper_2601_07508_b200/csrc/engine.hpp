@@ -53,6 +53,9 @@ void accumulate_host(double* C, i64 ldc, const double* A, i64 lda, const double*
 void block_gemm_mod_host(double* C, i64 ldc, const double* A, i64 lda, const double* B, i64 ldb,
                          i64 m, i64 k, i64 n, u64 lambda, u64 p, unsigned flags);
 
+// library-default engine for a product shape: FPMM_B200_ENGINE_I8 or _RNS
+unsigned select_engine(i64 m, i64 k, i64 n, u64 p);
+
 int device_count();
 void random_residues_device(double* dM, i64 ld, i64 rows, i64 cols, i64 row0, u64 p, u64 seed, int device,
                             void* stream);

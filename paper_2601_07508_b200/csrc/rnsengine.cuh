@@ -72,6 +72,7 @@ struct Params {
   int kb_per_split;  // split-K: k-blocks per slice
   int splits;
   int group;         // pair-tile rows per rasterisation group
+  int prefetch;      // L2 prefetch distance in k-blocks beyond the smem stages (0 = off)
   int dbg;           // experiments only (FPMM_B200_RNS_DEBUG): 1 = L2-resident operands, 2 = empty epilogue
   i64 split_stride;
   unsigned long long p, mu;            // Barrett: mu = floor(2^64 / p)
@@ -489,6 +490,13 @@ __device__ __forceinline__ uint64_t policy_evict_normal() {
   asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;\n" : "=l"(p));
   return p;
 }
+// L2 prefetch of one 8 KB chunk: extends the pipeline's latency cover
+// beyond the 12 shared-memory stages (DRAM misses of a phase's first touch)
+__device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap* map, int row) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n" ::"l"(reinterpret_cast<uint64_t>(map)),
+               "r"(0), "r"(row)
+               : "memory");
+}
 // arrive on the barrier at this offset in both CTAs of the pair once the MMAs issued so far completed
 __device__ __forceinline__ void commit_pair(uint64_t* bar) {
   asm volatile(
@@ -557,9 +565,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
           int rowA = static_cast<int>(((rb * P.nmod + i) * P.KB + kb0) * (kAStage / 128));
           int rowB = static_cast<int>(((cb * P.nmod + i) * P.KB + kb0) * (kBStage / 128));
           if (P.dbg & 1) rowA = rowB = static_cast<int>(rank) * 64 * 32;
+          if (P.prefetch > 0 && !(P.dbg & 1))
+            for (int kb = 0; kb < min(nkb, P.prefetch); ++kb) {
+              tma_prefetch_l2(&P.tmA, rowA + kb * (kAStage / 128));
+              tma_prefetch_l2(&P.tmB, rowB + kb * (kBStage / 128));
+            }
           for (int kb = 0; kb < nkb; ++kb, ++g) {
             const int s = g % kStages;
             if (g >= kStages) dev::mbar_wait(&empty[s], ((g / kStages) - 1) & 1);
+            if (P.prefetch > 0 && kb + P.prefetch < nkb && !(P.dbg & 1)) {
+              tma_prefetch_l2(&P.tmA, rowA + (kb + P.prefetch) * (kAStage / 128));
+              tma_prefetch_l2(&P.tmB, rowB + (kb + P.prefetch) * (kBStage / 128));
+            }
             if (rank == 0) dev::mbar_arrive_expect_tx(&full[s], 2 * kStageBytes);
             const int kq = (P.dbg & 1) ? (kb & 31) : kb;
             tma_pair_load(sA + s * kAStage, &P.tmA, rowA + kq * (kAStage / 128), &full[s], polA);

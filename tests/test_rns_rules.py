@@ -160,3 +160,18 @@ def test_packer_residue_split():
 def test_infeasible_range_raises():
     with pytest.raises(F.InfeasibleError):
         F.rns_plan(F.prev_prime(1 << 52), 1 << 60)
+
+
+@pytest.mark.parametrize("shape,bits,want", [
+    ((1024, 1024, 1024), 50, "i8"),         # C1: 16 pair tiles cannot fill 74 SM pairs
+    ((8192, 8192, 8192), 20, "rns"),        # C2 sweep: 7 moduli vs 9 digit products
+    ((8192, 8192, 8192), 52, "rns"),        # 15 vs 49
+    ((32768, 32768, 32768), 52, "rns"),     # C3
+    ((4096, 262144, 4096), 48, "rns"),      # C4
+    ((65536, 256, 65536), 40, "rns"),       # C5: the base-256 epilogue dominates at K = 256
+    ((10923, 32768, 32), 48, "i8"),         # unbalanced: n = 32 would waste 7/8 of an RNS tile
+])
+def test_default_engine_choice(shape, bits, want):
+    """The measured winner at each BASELINE config (profiles/round1/configs.json)."""
+    m, k, n = shape
+    assert F.select_engine(m, k, n, F.prev_prime(1 << bits)) == want

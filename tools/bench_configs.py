@@ -72,7 +72,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
     ap.add_argument("--only", default=",".join(CONFIGS))
-    ap.add_argument("--engines", default="i8,dmma")
+    ap.add_argument("--engines", default="auto,rns,i8,dmma")
     args = ap.parse_args()
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
