@@ -378,7 +378,7 @@ def main():
             "config": {"workload": args.workload, "m": m, "k": k, "n": n,
                        "bits": [bits_list[0], bits_list[-1]], "products_per_step": len(probs),
                        "rule": "plan_for_modulus (paper bound, b=2 scan fix)",
-                       "parallelism": "row-sharded x%d, NCCL bcast B words + gather C" % world,
+                       "parallelism": "row-sharded x%d, NCCL bcast of B (packed words or raw residues, the smaller) + gather C" % world,
                        "l2": "inputs (512 MiB/operand) larger than L2; no flush"},
             "engine": args.engine,
             "roofline": roof,

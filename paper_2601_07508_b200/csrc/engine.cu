@@ -935,6 +935,7 @@ void product_host(const ProductArgs& a, int ngpus, fpmm_b200_timing* tm) {
   // device 0 and broadcast over NCCL (NVLink); each device writes its C rows
   // straight back into the host matrix (row blocks are contiguous).
   g_all.ensure(ngpus);
+  const bool raw = (a.flags & FPMM_B200_BCAST_RAW_B) || j.bpack_bytes > static_cast<size_t>(8) * a.k * a.n;
   const i64 rows_per = part_rows(a.m, ngpus, j.BM);
   std::vector<i64> r0(ngpus), rn(ngpus);
   for (int g = 0; g < ngpus; ++g) {
@@ -968,16 +969,32 @@ void product_host(const ProductArgs& a, int ngpus, fpmm_b200_timing* tm) {
     }
     CUDA_OK(cudaEventRecord(c.ev[1], c.stream));
     if (rn[g] > 0) launch_pack_a(j, dA[g], a.k, rn[g], apack[g], errs[g], c.stream);
-    if (g == 0) launch_pack_b(j, dB0, a.n, bpack[0], errs[0], c.stream);
+    if (g == 0 && !raw) launch_pack_b(j, dB0, a.n, bpack[0], errs[0], c.stream);
     CUDA_OK(cudaEventRecord(c.ev[2], c.stream));
   }
+  // B crosses NVLink once, as packed words or (fewer bytes / BCAST_RAW_B) as raw residues packed per device
+  std::vector<double*> dBg(ngpus, dB0);
+  if (raw)
+    for (int g = 1; g < ngpus; ++g) {
+      CUDA_OK(cudaSetDevice(g));
+      dBg[g] = static_cast<double*>(cs[g]->b.get(sizeof(double) * a.k * a.n));
+    }
   NCCL_OK(nccl().GroupStart());
   for (int g = 0; g < ngpus; ++g) {
     CUDA_OK(cudaSetDevice(g));
-    NCCL_OK(nccl().Broadcast(bpack[0], bpack[g], j.bpack_bytes, ncclUint8, 0, g_all.comms[g], cs[g]->stream));
+    if (raw)
+      NCCL_OK(nccl().Broadcast(dB0, dBg[g], static_cast<size_t>(a.k * a.n), ncclDouble, 0, g_all.comms[g],
+                               cs[g]->stream));
+    else
+      NCCL_OK(nccl().Broadcast(bpack[0], bpack[g], j.bpack_bytes, ncclUint8, 0, g_all.comms[g], cs[g]->stream));
   }
   NCCL_OK(nccl().GroupEnd());
-  int nl = 1;
+  if (raw)
+    for (int g = 0; g < ngpus; ++g) {
+      CUDA_OK(cudaSetDevice(g));
+      launch_pack_b(j, dBg[g], a.n, bpack[g], g == 0 ? errs[0] : nullptr, cs[g]->stream);
+    }
+  int nl = raw ? ngpus : 1;
   for (int g = 0; g < ngpus; ++g) {
     DeviceCtx& c = *cs[g];
     CUDA_OK(cudaSetDevice(g));
@@ -1288,14 +1305,28 @@ void dist_product_device(const double* dA_rows, i64 lda, const double* dB, i64 l
     CUDA_OK(cudaMemsetAsync(err, 0, sizeof(int), s));
   }
   CUDA_OK(cudaEventRecord(c.ev[0], s));
-  if (g_dist.rank == root) launch_pack_b(j, dB, ldb, bpack, err, s);
-  if (rn > 0) launch_pack_a(j, dA_rows, lda, rn, apack, err, s);
-  CUDA_OK(cudaEventRecord(c.ev[1], s));
-  NCCL_OK(nccl().Broadcast(bpack, bpack, j.bpack_bytes, ncclUint8, root, g_dist.comm, s));
+  // B crosses NVLink once: as packed words, or as raw residues (8 B per
+  // element) packed by every rank when that is fewer bytes (the RNS engine
+  // above 8 moduli, the FP64 engine at v >= 2) or when BCAST_RAW_B asks
+  const bool raw = (flags & FPMM_B200_BCAST_RAW_B) || j.bpack_bytes > static_cast<size_t>(8) * k * n;
+  if (raw) {
+    double* dBd = static_cast<double*>(c.b.get(sizeof(double) * k * n));
+    if (g_dist.rank == root)
+      CUDA_OK(cudaMemcpy2DAsync(dBd, n * 8, dB, ldb * 8, n * 8, k, cudaMemcpyDeviceToDevice, s));
+    if (rn > 0) launch_pack_a(j, dA_rows, lda, rn, apack, err, s);
+    CUDA_OK(cudaEventRecord(c.ev[1], s));
+    NCCL_OK(nccl().Broadcast(dBd, dBd, static_cast<size_t>(k * n), ncclDouble, root, g_dist.comm, s));
+    launch_pack_b(j, dBd, n, bpack, g_dist.rank == root ? err : nullptr, s);
+  } else {
+    if (g_dist.rank == root) launch_pack_b(j, dB, ldb, bpack, err, s);
+    if (rn > 0) launch_pack_a(j, dA_rows, lda, rn, apack, err, s);
+    CUDA_OK(cudaEventRecord(c.ev[1], s));
+    NCCL_OK(nccl().Broadcast(bpack, bpack, j.bpack_bytes, ncclUint8, root, g_dist.comm, s));
+  }
   CUDA_OK(cudaEventRecord(c.ev[2], s));
   const int gl = rn > 0 ? launch_gemm(j, apack, bpack, dC_rows, ldc, rn, s) : 0;
   CUDA_OK(cudaEventRecord(c.ev[3], s));
-  int launches = (rn > 0 ? 1 + gl : 0) + (g_dist.rank == root ? 1 : 0);
+  int launches = (rn > 0 ? 1 + gl : 0) + (g_dist.rank == root || raw ? 1 : 0);
   if (dC_full) {
     // gather row blocks to root (grouped point-to-point; NCCL has no gather)
     if (ldc != n || (g_dist.rank == root && ldc_full != n))

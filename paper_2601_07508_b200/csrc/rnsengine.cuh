@@ -644,7 +644,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
         uint8_t* slot = P.scratch + (static_cast<i64>(t) * 2 + rank) * P.nmod * kSlotPerMod;
         for (int seg = 0; seg < nseg; ++seg, ++pass) {
           const int b = pass & 1;
-          dev::mbar_wait(&tmem_full[b], (pass >> 1) & 1);
+          if (P.dbg & 256) dev::mbar_wait(&tmem_full[b], (pass >> 1) & 1);
+          else dev::mbar_wait_sleep(&tmem_full[b], (pass >> 1) & 1, 256);
           i8::fence_after();
           const uint32_t tcol = tbase + tlane + b * kNT + half * (kNT / 2);
 #pragma unroll 1
