@@ -578,11 +578,8 @@ int launch_gemm_rns(const Job& j, const void* apack, const void* bpack, double* 
   const unsigned grid = 2 * static_cast<unsigned>(std::max<i64>(1, std::min<i64>(items, sms / 2)));
   // residue bytes of every item: n bytes per output element and slice
   q.scratch = static_cast<uint8_t*>(dc.scratch.get(static_cast<size_t>(items) * 2 * j.nmod * rns::kSlotPerMod));
-  if (const char* d = std::getenv("FPMM_B200_RNS_DEBUG")) q.dbg = std::atoi(d);
   q.group = rns::kGroup;
   if (const char* d = std::getenv("FPMM_B200_RNS_GROUP")) q.group = std::max(1, std::atoi(d));
-  q.prefetch = 0;
-  if (const char* d = std::getenv("FPMM_B200_RNS_PREFETCH")) q.prefetch = std::max(0, std::atoi(d));
   static bool configured[64] = {};
   if (!configured[dev & 63]) {
     CUDA_OK(cudaFuncSetAttribute(rns::rns_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, rns::kSmem));

@@ -4,27 +4,32 @@
 // of a positional base: every centred residue x' = x - p [x > p/2] is
 // represented by its residues modulo N pairwise-coprime moduli m_i <= 256
 // (one byte each).  The exact integer X = sum_k a'_k b'_k satisfies
-// |X| <= K floor(p/2)^2, so with M = prod m_i > 2.001 K floor(p/2)^2 it is
+// |X| <= K floor(p/2)^2, so with M = prod m_i >= 2.03 K floor(p/2)^2 it is
 // recovered from its residues r_i = X mod m_i by the CRT, and reduced mod p
 // without ever forming X:
 //   Z = sum_i r_i y_i M_i  (M_i = M/m_i, y_i = M_i^{-1} mod m_i),  Z = X + t M,
-//   t = round(sum_i r_i y_i / m_i)  (|X|/M < 1/2 - 2e-4, fixed point 2^-24),
+//   t = round(sum_i r_i y_i / m_i)  (|X|/M <= 1/2.03, fixed point 2^-19),
 //   X mod p = (sum_i r_i W_i - t (M mod p)) mod p,  W_i = y_i M_i mod p.
 // Each r_i is one exact int8 GEMM: T_i = A_i B_i (u8 x u8 -> s32 in TMEM,
 // exact while K_seg 255^2 < 2^32), r_i = T_i mod m_i.  N grows like
 // (2 bits(p) + log2 K) / 8 against D^2 = ceil(bits/8)^2 digit products for
 // the base-256 engine (15 vs 49 at 52 bits, K = 8192).
 //
-// One CTA computes a 128 x 256 tile of C, one modulus per pass (N passes),
-// M=128 N=256 K=32 MMAs into one of two 256-column TMEM accumulators, so the
-// epilogue of pass i overlaps the MMAs of pass i+1.  The epilogue reduces
-// T_i mod m_i and parks the residue bytes in a per-CTA L2 scratch slot; after
-// the last pass of the tile the same threads read their bytes back and run
-// the CRT above, storing C.  No product word ever reaches HBM.
+// Three kernels per product:
+//   pack_a_rns / pack_b_rns: the residues of every operand element modulo each
+//     m_i, written as canonical K-major UMMA chunks (one plane per modulus);
+//   rns_kernel: persistent CTA pairs (clusters of 2) computing 256 x 256 tiles
+//     with tcgen05.mma.cta_group::2.kind::i8, one modulus per pass, passes in
+//     modulus-major order over the grid; the epilogue reduces T_i mod m_i and
+//     parks one byte per element and modulus in HBM;
+//   rns_crt_kernel: the CRT above, from the parked bytes into C.
+// No int32 product leaves the SM; the parked residues are n bytes per output
+// element.
 //
-// Warp roles (10 warps): 0 TMA producer (1-D bulk copies of pre-packed
-// chunks), 1 TMEM allocator + single-thread MMA issuer, 2..9 epilogue (TMEM
-// lane quadrant w % 4, column half (w - 2) / 4).
+// rns_kernel warp roles (10 warps): 0 TMA producer (2-CTA tensor-map loads
+// completing on the leader's barrier), 1 TMEM allocator + (leader only) the
+// single-thread MMA issuer, 2..9 epilogue (TMEM lane quadrant w % 4, column
+// half (w - 2) / 4).
 #pragma once
 
 #include <cuda.h>
@@ -72,8 +77,6 @@ struct Params {
   int kb_per_split;  // split-K: k-blocks per slice
   int splits;
   int group;         // pair-tile rows per rasterisation group
-  int prefetch;      // L2 prefetch distance in k-blocks beyond the smem stages (0 = off)
-  int dbg;           // experiments only (FPMM_B200_RNS_DEBUG): 1 = L2-resident operands, 2 = empty epilogue
   i64 split_stride;
   unsigned long long p, mu;            // Barrett: mu = floor(2^64 / p)
   unsigned long long two32, two32_sh;  // 2^32 mod p and its Shoup quotient
@@ -242,7 +245,7 @@ __device__ __forceinline__ uint4* scratch_at(uint8_t* slot, int i, int half, int
 
 // Reduce 32 TMEM columns (one tcgen05.ld) mod m and park them as 2 x 16 bytes.
 __device__ __forceinline__ void park32(const uint32_t (&v)[32], uint32_t m, uint32_t negm, uint32_t c16, uint32_t magic,
-                                       bool acc, bool stream, uint4* dst0, uint4* dst1) {
+                                       bool acc, uint4* dst0, uint4* dst1) {
   uint32_t w[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
@@ -270,13 +273,9 @@ __device__ __forceinline__ void park32(const uint32_t (&v)[32], uint32_t m, uint
       w[q] = word;
     }
   }
-  if (stream) {  // read back only by the CRT kernel: keep them from evicting operand panels
-    __stcs(dst0, make_uint4(w[0], w[1], w[2], w[3]));
-    __stcs(dst1, make_uint4(w[4], w[5], w[6], w[7]));
-  } else {
-    *dst0 = make_uint4(w[0], w[1], w[2], w[3]);
-    *dst1 = make_uint4(w[4], w[5], w[6], w[7]);
-  }
+  // streaming stores: read back only by the CRT kernel
+  __stcs(dst0, make_uint4(w[0], w[1], w[2], w[3]));
+  __stcs(dst1, make_uint4(w[4], w[5], w[6], w[7]));
 }
 
 // ------------------------------------------------------------------ CRT
@@ -466,36 +465,13 @@ __device__ __forceinline__ void mma_i8_pair(uint32_t tmem_d, uint64_t adesc, uin
 // Pair TMA load of one 8 KB chunk (row `row` of the 128-byte view) into this
 // CTA's shared memory, completing on the LEADER's barrier at the same offset
 // (peer bit cleared), so the leader's one barrier tracks both halves.
-__device__ __forceinline__ void tma_pair_load(void* dst, const CUtensorMap* map, int row, uint64_t* bar,
-                                              uint64_t policy) {
+__device__ __forceinline__ void tma_pair_load(void* dst, const CUtensorMap* map, int row, uint64_t* bar) {
   const uint32_t leader_bar = dev::smem_u32(bar) & 0xFEFFFFFFu;
   asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
-      "[%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(dev::smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(row), "r"(leader_bar), "l"(policy)
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];\n" ::"r"(dev::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(row), "r"(leader_bar)
       : "memory");
-}
-__device__ __forceinline__ uint64_t policy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t policy_evict_normal() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;\n" : "=l"(p));
-  return p;
-}
-// L2 prefetch of one 8 KB chunk: extends the pipeline's latency cover
-// beyond the 12 shared-memory stages (DRAM misses of a phase's first touch)
-__device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap* map, int row) {
-  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n" ::"l"(reinterpret_cast<uint64_t>(map)),
-               "r"(0), "r"(row)
-               : "memory");
 }
 // arrive on the barrier at this offset in both CTAs of the pair once the MMAs issued so far completed
 __device__ __forceinline__ void commit_pair(uint64_t* bar) {
@@ -552,9 +528,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
     // The leader's full[s] expects both CTAs' bytes; each CTA's loads
     // complete on it, so the leader's one wait covers the pair.
     if (lane == 0) {
-      // (evict_last for A / evict_first for B measured 2-10% slower than normal)
-      const uint64_t polA = (P.dbg & 128) ? policy_evict_last() : policy_evict_normal();
-      const uint64_t polB = (P.dbg & 128) ? policy_evict_first() : policy_evict_normal();
+      // (measured and rejected: L2 evict_last/evict_first hints for A/B, -2..10%;
+      // cp.async.bulk.prefetch.L2 8..64 k-blocks ahead, -9..19%)
       int g = 0;
       for (int i = 0; i < P.nmod; ++i) {
         for (int t = pair; t < total; t += npairs) {
@@ -562,25 +537,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
           const int kb0 = it.ks * P.kb_per_split;
           const int nkb = max(0, min(P.KB, kb0 + P.kb_per_split) - kb0);
           const i64 rb = 2 * static_cast<i64>(it.tm) + rank, cb = 2 * static_cast<i64>(it.tn) + rank;
-          int rowA = static_cast<int>(((rb * P.nmod + i) * P.KB + kb0) * (kAStage / 128));
-          int rowB = static_cast<int>(((cb * P.nmod + i) * P.KB + kb0) * (kBStage / 128));
-          if (P.dbg & 1) rowA = rowB = static_cast<int>(rank) * 64 * 32;
-          if (P.prefetch > 0 && !(P.dbg & 1))
-            for (int kb = 0; kb < min(nkb, P.prefetch); ++kb) {
-              tma_prefetch_l2(&P.tmA, rowA + kb * (kAStage / 128));
-              tma_prefetch_l2(&P.tmB, rowB + kb * (kBStage / 128));
-            }
+          const int rowA = static_cast<int>(((rb * P.nmod + i) * P.KB + kb0) * (kAStage / 128));
+          const int rowB = static_cast<int>(((cb * P.nmod + i) * P.KB + kb0) * (kBStage / 128));
           for (int kb = 0; kb < nkb; ++kb, ++g) {
             const int s = g % kStages;
             if (g >= kStages) dev::mbar_wait(&empty[s], ((g / kStages) - 1) & 1);
-            if (P.prefetch > 0 && kb + P.prefetch < nkb && !(P.dbg & 1)) {
-              tma_prefetch_l2(&P.tmA, rowA + (kb + P.prefetch) * (kAStage / 128));
-              tma_prefetch_l2(&P.tmB, rowB + (kb + P.prefetch) * (kBStage / 128));
-            }
             if (rank == 0) dev::mbar_arrive_expect_tx(&full[s], 2 * kStageBytes);
-            const int kq = (P.dbg & 1) ? (kb & 31) : kb;
-            tma_pair_load(sA + s * kAStage, &P.tmA, rowA + kq * (kAStage / 128), &full[s], polA);
-            tma_pair_load(sB + s * kBStage, &P.tmB, rowB + kq * (kBStage / 128), &full[s], polB);
+            tma_pair_load(sA + s * kAStage, &P.tmA, rowA + kb * (kAStage / 128), &full[s]);
+            tma_pair_load(sB + s * kBStage, &P.tmB, rowB + kb * (kBStage / 128), &full[s]);
           }
         }
       }
@@ -644,8 +608,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
         uint8_t* slot = P.scratch + (static_cast<i64>(t) * 2 + rank) * P.nmod * kSlotPerMod;
         for (int seg = 0; seg < nseg; ++seg, ++pass) {
           const int b = pass & 1;
-          if (P.dbg & 256) dev::mbar_wait(&tmem_full[b], (pass >> 1) & 1);
-          else dev::mbar_wait_sleep(&tmem_full[b], (pass >> 1) & 1, 256);
+          dev::mbar_wait_sleep(&tmem_full[b], (pass >> 1) & 1, 256);
           i8::fence_after();
           const uint32_t tcol = tbase + tlane + b * kNT + half * (kNT / 2);
 #pragma unroll 1
@@ -658,8 +621,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
               __syncwarp();
               if (lane == 0) mbar_arrive_cluster(leader_tmem_empty + b * 8);
             }
-            if (!(P.dbg & 10))
-              park32(v, m, nm, c16, mg, seg > 0, !(P.dbg & 32), scratch_at(slot, i, half, c0 / 16, row_in_tile),
+            park32(v, m, nm, c16, mg, seg > 0, scratch_at(slot, i, half, c0 / 16, row_in_tile),
                      scratch_at(slot, i, half, c0 / 16 + 1, row_in_tile));
           }
         }
