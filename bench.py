@@ -251,7 +251,7 @@ def main():
                                     timing=tm if record is not None else None)
                 launches[0] += per_launch.get(b, 0)
             if record is not None:
-                record[b] = (tm.gemm_ms, tm.engine, tm.words, tm.launches)
+                record[b] = (tm.gemm_ms, tm.engine, tm.words, tm.launches, tm.recon_ms, tm.pack_ms)
 
     def barrier():
         if world > 1:
@@ -310,7 +310,7 @@ def main():
         work = gemm_total = 0.0
         ran = set()
         for (b, p, u, v, lam, lk) in probs:
-            g, e_ran, words, _ = rec[b]
+            g, e_ran, words, _, recon, packt = rec[b]
             ran.add(e_ran)
             rn = rows[b][1]
             if e_ran == F.ENGINE_DMMA:
@@ -326,6 +326,7 @@ def main():
             gemm_total += g
             pk = "dmma" if e_ran == F.ENGINE_DMMA else "i8"
             per_bits[str(b)] = dict({"u": u, "v": v, "lambda": lam, "gemm_ms": round(g, 3),
+                                     "pack_ms": round(packt, 3), "recon_ms": round(recon, 3),
                                      "eff_gflops": round(2.0 * rn * k * n / (g * 1e-3) / 1e9, 1),
                                      "tensor_frac": round(w / (g * 1e-3) / 1e12 / peaks[pk], 4)}, **extra)
         achieved = work / (gemm_total * 1e-3) / 1e12

@@ -87,6 +87,8 @@ typedef struct {
   int32_t ngpus;       /* devices used                                       */
   int32_t engine;      /* engine that ran: 0x10 DMMA, 0x20 I8, 0x40 RNS (FPMM_B200_ENGINE_*) */
   int32_t words;       /* words per residue: u*v (DMMA), base-256 digits D (I8), moduli (RNS) */
+  double recon_ms;     /* reconstruction kernels after the product kernel (RNS CRT, int8 split-K
+                          combine); gemm_ms is the product kernel alone where this is set */
 } fpmm_b200_timing;
 
 /* ------------------------------------------------------------ diagnostics */

@@ -100,7 +100,7 @@ class Timing(C.Structure):
     _fields_ = [("h2d_ms", C.c_double), ("pack_ms", C.c_double), ("gemm_ms", C.c_double),
                 ("comm_ms", C.c_double), ("d2h_ms", C.c_double), ("total_ms", C.c_double),
                 ("lambda_k", C.c_int64), ("launches", C.c_int32), ("ngpus", C.c_int32),
-                ("engine", C.c_int32), ("words", C.c_int32)]
+                ("engine", C.c_int32), ("words", C.c_int32), ("recon_ms", C.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -455,7 +455,7 @@ void launch_pack_b(const Job& j, const double* B, i64 ldb, void* bpack, int* err
 }
 
 int launch_gemm_i8(const Job& j, const void* apack, const void* bpack, double* C, i64 ldc, i64 rows,
-                   cudaStream_t s) {
+                   cudaStream_t s, cudaEvent_t mid) {
   i8::Params q = j.ip;
   q.apack = static_cast<const uint8_t*>(apack);
   q.bpack = static_cast<const uint8_t*>(bpack);
@@ -509,6 +509,7 @@ int launch_gemm_i8(const Job& j, const void* apack, const void* bpack, double* C
     kern<<<grid, i8::kThreads, CF::kSmem, s>>>(q);
   });
   CUDA_OK(cudaGetLastError());
+  if (mid) CUDA_OK(cudaEventRecord(mid, s));
   if (splits > 1) {
     i8::splitk_reduce_kernel<<<grid_for(rows * j.n, 256), 256, 0, s>>>(work, rows * j.n, splits, C, ldc, rows,
                                                                         j.n, j.p);
@@ -543,7 +544,7 @@ CUtensorMap chunk_map(const void* base, size_t bytes) {
 }
 
 int launch_gemm_rns(const Job& j, const void* apack, const void* bpack, double* C, i64 ldc, i64 rows,
-                    cudaStream_t s) {
+                    cudaStream_t s, cudaEvent_t mid) {
   rns::Params q = j.rp;
   q.apack = static_cast<const uint8_t*>(apack);
   q.bpack = static_cast<const uint8_t*>(bpack);
@@ -587,6 +588,7 @@ int launch_gemm_rns(const Job& j, const void* apack, const void* bpack, double* 
   }
   rns::rns_kernel<<<grid, rns::kThreads, rns::kSmem, s>>>(q);
   CUDA_OK(cudaGetLastError());
+  if (mid) CUDA_OK(cudaEventRecord(mid, s));
   // CRT of every tile (slices summed mod m_i first) straight into C
   rns::CrtParams cp = j.rcp;
   cp.R = q.scratch;
@@ -602,10 +604,12 @@ int launch_gemm_rns(const Job& j, const void* apack, const void* bpack, double* 
 }
 
 // Launches the product kernel(s) for packed operands; returns the launch count.
+// `mid` (nullable) is recorded after the product kernel, before any
+// reconstruction kernel (RNS CRT, int8 split-K combine).
 int launch_gemm(const Job& j, const void* apack_v, const void* bpack_v, double* C, i64 ldc, i64 rows,
-                cudaStream_t s) {
-  if (j.engine == kRns) return launch_gemm_rns(j, apack_v, bpack_v, C, ldc, rows, s);
-  if (j.engine == kI8) return launch_gemm_i8(j, apack_v, bpack_v, C, ldc, rows, s);
+                cudaStream_t s, cudaEvent_t mid = nullptr) {
+  if (j.engine == kRns) return launch_gemm_rns(j, apack_v, bpack_v, C, ldc, rows, s, mid);
+  if (j.engine == kI8) return launch_gemm_i8(j, apack_v, bpack_v, C, ldc, rows, s, mid);
   const double* apack = static_cast<const double*>(apack_v);
   const double* bpack = static_cast<const double*>(bpack_v);
   GemmParams g = j.gp;
@@ -630,6 +634,7 @@ int launch_gemm(const Job& j, const void* apack_v, const void* bpack_v, double* 
     kern<<<static_cast<unsigned>(tiles), Cfg::kThreads, Cfg::kSmem, s>>>(g);
   });
   CUDA_OK(cudaGetLastError());
+  if (mid) CUDA_OK(cudaEventRecord(mid, s));
   return 1;
 }
 
@@ -707,13 +712,14 @@ void product_device(const ProductArgs& a, int device, void* stream, fpmm_b200_ti
   launch_pack_a(j, a.A, a.lda, a.m, apack, err, s);
   launch_pack_b(j, a.B, a.ldb, bpack, err, s);
   if (tm) CUDA_OK(cudaEventRecord(c.ev[1], s));
-  const int gl = launch_gemm(j, apack, bpack, a.C, a.ldc, a.m, s);
+  const int gl = launch_gemm(j, apack, bpack, a.C, a.ldc, a.m, s, tm ? c.ev[5] : nullptr);
   if (tm) CUDA_OK(cudaEventRecord(c.ev[2], s));
   if (err) check_err_flag(c, s);
   if (tm) {
     CUDA_OK(cudaEventSynchronize(c.ev[2]));
     tm->pack_ms = elapsed(c.ev[0], c.ev[1]);
-    tm->gemm_ms = elapsed(c.ev[1], c.ev[2]);
+    tm->gemm_ms = elapsed(c.ev[1], c.ev[5]);
+    tm->recon_ms = elapsed(c.ev[5], c.ev[2]);
     tm->total_ms = elapsed(c.ev[0], c.ev[2]);
     tm->lambda_k = j.lambda_k;
     tm->engine = engine_flag(j), tm->words = engine_words(j);
@@ -802,13 +808,14 @@ void product_prepared_device(const Prepared* h, const double* dB, i64 ldb, doubl
   if (tm) CUDA_OK(cudaEventRecord(c.ev[0], s));
   launch_pack_b(j, dB, ldb, bpack, err, s);
   if (tm) CUDA_OK(cudaEventRecord(c.ev[1], s));
-  const int gl = launch_gemm(j, h->words.ptr, bpack, dC, ldc, h->m, s);
+  const int gl = launch_gemm(j, h->words.ptr, bpack, dC, ldc, h->m, s, tm ? c.ev[5] : nullptr);
   if (tm) CUDA_OK(cudaEventRecord(c.ev[2], s));
   if (err) check_err_flag(c, s);
   if (tm) {
     CUDA_OK(cudaEventSynchronize(c.ev[2]));
     tm->pack_ms = elapsed(c.ev[0], c.ev[1]);
-    tm->gemm_ms = elapsed(c.ev[1], c.ev[2]);
+    tm->gemm_ms = elapsed(c.ev[1], c.ev[5]);
+    tm->recon_ms = elapsed(c.ev[5], c.ev[2]);
     tm->total_ms = elapsed(c.ev[0], c.ev[2]);
     tm->lambda_k = j.lambda_k;
     tm->engine = engine_flag(j), tm->words = engine_words(j);
