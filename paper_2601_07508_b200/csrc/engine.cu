@@ -61,12 +61,38 @@ struct DevBuf {
   }
 };
 
+// Device workspaces of one product in flight: packed words, the RNS residue
+// blocks and the split-K partials.  Products issued on different streams get
+// different sets, so independent products overlap on the device (the packs
+// and reconstruction of one run beside the tensor-core kernel of another).
+struct Workspace {
+  DevBuf apack, bpack, scratch, splitws;
+  void release() { apack.release(), bpack.release(), scratch.release(), splitws.release(); }
+};
+
 struct DeviceCtx {
   static constexpr int kChunks = 16;  // host-path pipeline depth (exposed head/tail ~1/16 of a product)
+  static constexpr int kStreamSets = 8;
   int dev = -1;
   cudaStream_t stream = nullptr, s_in = nullptr, s_out = nullptr;
   cudaEvent_t ev[8] = {}, ev_in[kChunks] = {}, ev_out[kChunks] = {};
-  DevBuf apack, bpack, a, b, c, tmp, err, splitws, scratch;
+  DevBuf a, b, c, tmp, err;
+  Workspace ws0;  // the library's own stream and the legacy default stream
+  std::vector<std::pair<cudaStream_t, std::unique_ptr<Workspace>>> ws_streams;
+  Workspace& ws_for(cudaStream_t s) {
+    if (s == nullptr || s == stream) return ws0;
+    for (auto& e : ws_streams)
+      if (e.first == s) return *e.second;
+    if (static_cast<int>(ws_streams.size()) >= kStreamSets) {
+      // a stream handle may be gone: only reuse a set once nothing is in flight
+      CUDA_OK(cudaDeviceSynchronize());
+      ws_streams.front().first = s;
+      std::rotate(ws_streams.begin(), ws_streams.begin() + 1, ws_streams.end());
+      return *ws_streams.back().second;
+    }
+    ws_streams.emplace_back(s, std::make_unique<Workspace>());
+    return *ws_streams.back().second;
+  }
   void init(int d) {
     dev = d;
     CUDA_OK(cudaSetDevice(d));
@@ -89,9 +115,10 @@ struct DeviceCtx {
     if (s_in) cudaStreamDestroy(s_in), s_in = nullptr;
     if (s_out) cudaStreamDestroy(s_out), s_out = nullptr;
     if (stream) cudaStreamDestroy(stream), stream = nullptr;
-    apack.release(), bpack.release(), a.release(), b.release(), c.release(), tmp.release(), err.release();
-    splitws.release();
-    scratch.release();
+    a.release(), b.release(), c.release(), tmp.release(), err.release();
+    ws0.release();
+    for (auto& e : ws_streams) e.second->release();
+    ws_streams.clear();
     dev = -1;
   }
 };
@@ -455,7 +482,7 @@ void launch_pack_b(const Job& j, const double* B, i64 ldb, void* bpack, int* err
 }
 
 int launch_gemm_i8(const Job& j, const void* apack, const void* bpack, double* C, i64 ldc, i64 rows,
-                   cudaStream_t s, cudaEvent_t mid) {
+                   cudaStream_t s, cudaEvent_t mid, Workspace& ws) {
   i8::Params q = j.ip;
   q.apack = static_cast<const uint8_t*>(apack);
   q.bpack = static_cast<const uint8_t*>(bpack);
@@ -482,10 +509,9 @@ int launch_gemm_i8(const Job& j, const void* apack, const void* bpack, double* C
   q.splits = splits;
   int dev = 0;
   CUDA_OK(cudaGetDevice(&dev));
-  DeviceCtx& dc = ctx(dev);
   double* work = nullptr;
   if (splits > 1) {
-    work = static_cast<double*>(dc.splitws.get(sizeof(double) * splits * rows * j.n));
+    work = static_cast<double*>(ws.splitws.get(sizeof(double) * splits * rows * j.n));
     q.C = work;
     q.ldc = j.n;
     q.split_stride = rows * j.n;
@@ -544,7 +570,7 @@ CUtensorMap chunk_map(const void* base, size_t bytes) {
 }
 
 int launch_gemm_rns(const Job& j, const void* apack, const void* bpack, double* C, i64 ldc, i64 rows,
-                    cudaStream_t s, cudaEvent_t mid) {
+                    cudaStream_t s, cudaEvent_t mid, Workspace& ws) {
   rns::Params q = j.rp;
   q.apack = static_cast<const uint8_t*>(apack);
   q.bpack = static_cast<const uint8_t*>(bpack);
@@ -570,7 +596,6 @@ int launch_gemm_rns(const Job& j, const void* apack, const void* bpack, double* 
   q.splits = splits;
   int dev = 0;
   CUDA_OK(cudaGetDevice(&dev));
-  DeviceCtx& dc = ctx(dev);
   int sms = 148;
   CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const i64 items = static_cast<i64>(q.MB) * q.NB * splits;
@@ -578,7 +603,7 @@ int launch_gemm_rns(const Job& j, const void* apack, const void* bpack, double* 
   // persistent CTA pairs (clusters of 2 on neighbouring SMs)
   const unsigned grid = 2 * static_cast<unsigned>(std::max<i64>(1, std::min<i64>(items, sms / 2)));
   // residue bytes of every item: n bytes per output element and slice
-  q.scratch = static_cast<uint8_t*>(dc.scratch.get(static_cast<size_t>(items) * 2 * j.nmod * rns::kSlotPerMod));
+  q.scratch = static_cast<uint8_t*>(ws.scratch.get(static_cast<size_t>(items) * 2 * j.nmod * rns::kSlotPerMod));
   q.group = rns::kGroup;
   if (const char* d = std::getenv("FPMM_B200_RNS_GROUP")) q.group = std::max(1, std::atoi(d));
   static bool configured[64] = {};
@@ -607,9 +632,9 @@ int launch_gemm_rns(const Job& j, const void* apack, const void* bpack, double* 
 // `mid` (nullable) is recorded after the product kernel, before any
 // reconstruction kernel (RNS CRT, int8 split-K combine).
 int launch_gemm(const Job& j, const void* apack_v, const void* bpack_v, double* C, i64 ldc, i64 rows,
-                cudaStream_t s, cudaEvent_t mid = nullptr) {
-  if (j.engine == kRns) return launch_gemm_rns(j, apack_v, bpack_v, C, ldc, rows, s, mid);
-  if (j.engine == kI8) return launch_gemm_i8(j, apack_v, bpack_v, C, ldc, rows, s, mid);
+                cudaStream_t s, Workspace& ws, cudaEvent_t mid = nullptr) {
+  if (j.engine == kRns) return launch_gemm_rns(j, apack_v, bpack_v, C, ldc, rows, s, mid, ws);
+  if (j.engine == kI8) return launch_gemm_i8(j, apack_v, bpack_v, C, ldc, rows, s, mid, ws);
   const double* apack = static_cast<const double*>(apack_v);
   const double* bpack = static_cast<const double*>(bpack_v);
   GemmParams g = j.gp;
@@ -701,8 +726,9 @@ void product_device(const ProductArgs& a, int device, void* stream, fpmm_b200_ti
     return;
   }
   const Job j = make_job(a.m, a.k, a.n, a.p, a.u, a.v, resolve_engine(a.flags));
-  void* apack = c.apack.get(j.apack_bytes);
-  void* bpack = c.bpack.get(j.bpack_bytes);
+  Workspace& ws = c.ws_for(s);
+  void* apack = ws.apack.get(j.apack_bytes);
+  void* bpack = ws.bpack.get(j.bpack_bytes);
   int* err = nullptr;
   if (a.flags & FPMM_B200_CHECK_INPUTS) {
     err = static_cast<int*>(c.err.get(sizeof(int)));
@@ -712,7 +738,7 @@ void product_device(const ProductArgs& a, int device, void* stream, fpmm_b200_ti
   launch_pack_a(j, a.A, a.lda, a.m, apack, err, s);
   launch_pack_b(j, a.B, a.ldb, bpack, err, s);
   if (tm) CUDA_OK(cudaEventRecord(c.ev[1], s));
-  const int gl = launch_gemm(j, apack, bpack, a.C, a.ldc, a.m, s, tm ? c.ev[5] : nullptr);
+  const int gl = launch_gemm(j, apack, bpack, a.C, a.ldc, a.m, s, ws, tm ? c.ev[5] : nullptr);
   if (tm) CUDA_OK(cudaEventRecord(c.ev[2], s));
   if (err) check_err_flag(c, s);
   if (tm) {
@@ -799,7 +825,8 @@ void product_prepared_device(const Prepared* h, const double* dB, i64 ldb, doubl
     return;
   }
   const Job j = make_job(h->m, h->k, n, h->p, h->u, h->v, h->engine);
-  void* bpack = c.bpack.get(j.bpack_bytes);
+  Workspace& ws = c.ws_for(s);
+  void* bpack = ws.bpack.get(j.bpack_bytes);
   int* err = nullptr;
   if (fl & FPMM_B200_CHECK_INPUTS) {
     err = static_cast<int*>(c.err.get(sizeof(int)));
@@ -808,7 +835,7 @@ void product_prepared_device(const Prepared* h, const double* dB, i64 ldb, doubl
   if (tm) CUDA_OK(cudaEventRecord(c.ev[0], s));
   launch_pack_b(j, dB, ldb, bpack, err, s);
   if (tm) CUDA_OK(cudaEventRecord(c.ev[1], s));
-  const int gl = launch_gemm(j, h->words.ptr, bpack, dC, ldc, h->m, s, tm ? c.ev[5] : nullptr);
+  const int gl = launch_gemm(j, h->words.ptr, bpack, dC, ldc, h->m, s, ws, tm ? c.ev[5] : nullptr);
   if (tm) CUDA_OK(cudaEventRecord(c.ev[2], s));
   if (err) check_err_flag(c, s);
   if (tm) {
@@ -880,8 +907,8 @@ void product_host(const ProductArgs& a, int ngpus, fpmm_b200_timing* tm) {
     double* dA = static_cast<double*>(c.a.get(sizeof(double) * a.m * a.k));
     double* dB = static_cast<double*>(c.b.get(sizeof(double) * a.k * a.n));
     double* dC = static_cast<double*>(c.c.get(sizeof(double) * a.m * a.n));
-    uint8_t* apack = static_cast<uint8_t*>(c.apack.get(j.apack_bytes));
-    void* bpack = c.bpack.get(j.bpack_bytes);
+    uint8_t* apack = static_cast<uint8_t*>(c.ws0.apack.get(j.apack_bytes));
+    void* bpack = c.ws0.bpack.get(j.bpack_bytes);
     const size_t per_rb = j.per_rb_bytes;
     // ~8 chunks of whole GEMM row tiles once the operands are large enough to matter
     const i64 bytes = 8 * (a.m * a.k + a.m * a.n);
@@ -913,7 +940,7 @@ void product_host(const ProductArgs& a, int ngpus, fpmm_b200_timing* tm) {
       uint8_t* ap = apack + static_cast<size_t>(r0 / j.BM) * per_rb;
       CUDA_OK(cudaStreamWaitEvent(s, c.ev_in[i], 0));
       launch_pack_a(j, dA + r0 * a.k, a.k, rn, ap, err, s);
-      nl += 1 + launch_gemm(j, ap, bpack, dC + r0 * a.n, a.n, rn, s);
+      nl += 1 + launch_gemm(j, ap, bpack, dC + r0 * a.n, a.n, rn, s, c.ws0);
       CUDA_OK(cudaEventRecord(c.ev_out[i], s));
       CUDA_OK(cudaStreamWaitEvent(so, c.ev_out[i], 0));
       CUDA_OK(cudaMemcpy2DAsync(a.C + r0 * a.ldc, a.ldc * 8, dC + r0 * a.n, a.n * 8, a.n * 8, rn,
@@ -957,8 +984,8 @@ void product_host(const ProductArgs& a, int ngpus, fpmm_b200_timing* tm) {
     CUDA_OK(cudaSetDevice(g));
     dA[g] = static_cast<double*>(c.a.get(sizeof(double) * std::max<i64>(rn[g], 1) * a.k));
     dC[g] = static_cast<double*>(c.c.get(sizeof(double) * std::max<i64>(rn[g], 1) * a.n));
-    apack[g] = c.apack.get(j.apack_bytes);
-    bpack[g] = c.bpack.get(j.bpack_bytes);
+    apack[g] = c.ws0.apack.get(j.apack_bytes);
+    bpack[g] = c.ws0.bpack.get(j.bpack_bytes);
     if (chk) {
       errs[g] = static_cast<int*>(c.err.get(sizeof(int)));
       CUDA_OK(cudaMemsetAsync(errs[g], 0, sizeof(int), c.stream));
@@ -1003,7 +1030,7 @@ void product_host(const ProductArgs& a, int ngpus, fpmm_b200_timing* tm) {
     DeviceCtx& c = *cs[g];
     CUDA_OK(cudaSetDevice(g));
     CUDA_OK(cudaEventRecord(c.ev[3], c.stream));
-    if (rn[g] > 0) nl += 1 + launch_gemm(j, apack[g], bpack[g], dC[g], a.n, rn[g], c.stream);
+    if (rn[g] > 0) nl += 1 + launch_gemm(j, apack[g], bpack[g], dC[g], a.n, rn[g], c.stream, c.ws0);
     CUDA_OK(cudaEventRecord(c.ev[4], c.stream));
     if (rn[g] > 0)
       CUDA_OK(cudaMemcpy2DAsync(a.C + r0[g] * a.ldc, a.ldc * 8, dC[g], a.n * 8, a.n * 8, rn[g],
@@ -1301,8 +1328,9 @@ void dist_product_device(const double* dA_rows, i64 lda, const double* dB, i64 l
   const Job j = make_job(m, k, n, p, u, v, resolve_engine(flags));
   i64 r0 = 0, rn = 0;
   dist_rows(m, g_dist.nranks, g_dist.rank, u, v, &r0, &rn);
-  void* apack = c.apack.get(j.apack_bytes);
-  void* bpack = c.bpack.get(j.bpack_bytes);
+  Workspace& ws = c.ws_for(s);
+  void* apack = ws.apack.get(j.apack_bytes);
+  void* bpack = ws.bpack.get(j.bpack_bytes);
   int* err = nullptr;
   if (flags & FPMM_B200_CHECK_INPUTS) {
     err = static_cast<int*>(c.err.get(sizeof(int)));
@@ -1328,7 +1356,7 @@ void dist_product_device(const double* dA_rows, i64 lda, const double* dB, i64 l
     NCCL_OK(nccl().Broadcast(bpack, bpack, j.bpack_bytes, ncclUint8, root, g_dist.comm, s));
   }
   CUDA_OK(cudaEventRecord(c.ev[2], s));
-  const int gl = rn > 0 ? launch_gemm(j, apack, bpack, dC_rows, ldc, rn, s) : 0;
+  const int gl = rn > 0 ? launch_gemm(j, apack, bpack, dC_rows, ldc, rn, s, ws) : 0;
   CUDA_OK(cudaEventRecord(c.ev[3], s));
   int launches = (rn > 0 ? 1 + gl : 0) + (g_dist.rank == root || raw ? 1 : 0);
   if (dC_full) {
