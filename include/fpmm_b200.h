@@ -56,6 +56,10 @@ typedef enum {
 #define FPMM_B200_ENGINE_DMMA 0x10u
 #define FPMM_B200_ENGINE_I8 0x20u
 #define FPMM_B200_ENGINE_RNS 0x40u
+/* FP64 engine: use exactly the caller's (u,v) words.  By default the engine may
+ * use other word counts where the caller's collapse the exact K-block
+ * (lambda_k = 4 at the rule's limits, e.g. (2,2) at 52 bits); C is the same. */
+#define FPMM_B200_DMMA_EXACT_WORDS 0x80u
 
 /* product variants (multiword.hpp:113-254); all map to the same fused kernel */
 typedef enum {

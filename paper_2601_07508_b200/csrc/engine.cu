@@ -12,6 +12,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "i8engine.cuh"
@@ -366,7 +367,30 @@ Job make_rns_job(i64 m, i64 k, i64 n, u64 p) {
   return j;
 }
 
-Job make_job(i64 m, i64 k, i64 n, u64 p, int u, int v, int engine = kDmma) {
+// FP64 engine word counts.  The engine's balanced signed words are internal
+// (C is the same for any counts), so at the rule's lambda-collapse points --
+// (2,2) at 52 bits, (1,3) at 39, (1,2) at 35, where the in-register
+// reduction every lambda_k = 4 terms caps the FP64 pipe at 4/7 -- a larger
+// count with a long exact block is cheaper: cost = u'v' (lambda_k + 3) /
+// lambda_k DMMA-equivalents per term (3 FP64-pipe ops per reduction).
+std::pair<int, int> dmma_words(u64 p, int u, int v, bool exact) {
+  if (exact) return {u, v};
+  auto cost = [&](int uu, int vv) {
+    const i64 lk = kernel_block(p, uu, vv, 4);
+    return lk < 4 ? 1e30 : uu * vv * (static_cast<double>(lk) + 3.0) / static_cast<double>(lk);
+  };
+  std::pair<int, int> best{u, v};
+  double bc = cost(u, v);
+  static constexpr int kCombos[12][2] = {{1, 1}, {1, 2}, {2, 1}, {1, 3}, {3, 1}, {1, 4},
+                                         {4, 1}, {2, 2}, {2, 3}, {3, 2}, {2, 4}, {4, 2}};
+  for (const auto& c : kCombos) {
+    const double cc = cost(c[0], c[1]);
+    if (cc < 0.97 * bc) bc = cc, best = {c[0], c[1]};  // only a clear win replaces the caller's words
+  }
+  return best;
+}
+
+Job make_job(i64 m, i64 k, i64 n, u64 p, int u, int v, int engine = kDmma, bool exact_words = false) {
   if (engine == kAuto) engine = auto_engine(m, k, n, p);
   if (engine == kRns) {
     Job j = make_rns_job(m, k, n, p);
@@ -378,6 +402,7 @@ Job make_job(i64 m, i64 k, i64 n, u64 p, int u, int v, int engine = kDmma) {
     j.u = u, j.v = v;
     return j;
   }
+  std::tie(u, v) = dmma_words(p, u, v, exact_words);
   Job j;
   j.m = m, j.k = k, j.n = n, j.p = p, j.u = u, j.v = v;
   dispatch(u, v, [&]<int U, int V, int MT, int NT>() {
@@ -725,7 +750,8 @@ void product_device(const ProductArgs& a, int device, void* stream, fpmm_b200_ti
     if (!(a.flags & FPMM_B200_ASYNC)) CUDA_OK(cudaStreamSynchronize(s));
     return;
   }
-  const Job j = make_job(a.m, a.k, a.n, a.p, a.u, a.v, resolve_engine(a.flags));
+  const Job j = make_job(a.m, a.k, a.n, a.p, a.u, a.v, resolve_engine(a.flags),
+                     (a.flags & FPMM_B200_DMMA_EXACT_WORDS) != 0);
   Workspace& ws = c.ws_for(s);
   void* apack = ws.apack.get(j.apack_bytes);
   void* bpack = ws.bpack.get(j.bpack_bytes);
@@ -783,7 +809,7 @@ Prepared* prepare_a_device(const double* dA, i64 lda, i64 m, i64 k, u64 p, int u
   if (h->engine == kAuto) h->engine = kI8;
   h->flags = flags;
   if (m > 0 && k > 0) {
-    const Job j = make_job(m, k, 1, p, u, v, h->engine);
+    const Job j = make_job(m, k, 1, p, u, v, h->engine, (flags & FPMM_B200_DMMA_EXACT_WORDS) != 0);
     void* w = h->words.get(j.apack_bytes);
     int* err = nullptr;
     if (flags & FPMM_B200_CHECK_INPUTS) {
@@ -824,7 +850,7 @@ void product_prepared_device(const Prepared* h, const double* dB, i64 ldb, doubl
     if (!(fl & FPMM_B200_ASYNC)) CUDA_OK(cudaStreamSynchronize(s));
     return;
   }
-  const Job j = make_job(h->m, h->k, n, h->p, h->u, h->v, h->engine);
+  const Job j = make_job(h->m, h->k, n, h->p, h->u, h->v, h->engine, (h->flags & FPMM_B200_DMMA_EXACT_WORDS) != 0);
   Workspace& ws = c.ws_for(s);
   void* bpack = ws.bpack.get(j.bpack_bytes);
   int* err = nullptr;
@@ -895,7 +921,8 @@ void product_host(const ProductArgs& a, int ngpus, fpmm_b200_timing* tm) {
     for (i64 r = 0; r < a.m; ++r) std::memset(a.C + r * a.ldc, 0, sizeof(double) * a.n);
     return;
   }
-  const Job j = make_job(a.m, a.k, a.n, a.p, a.u, a.v, resolve_engine(a.flags));
+  const Job j = make_job(a.m, a.k, a.n, a.p, a.u, a.v, resolve_engine(a.flags),
+                     (a.flags & FPMM_B200_DMMA_EXACT_WORDS) != 0);
   const unsigned chk = a.flags & FPMM_B200_CHECK_INPUTS;
 
   if (ngpus == 1) {
@@ -1325,7 +1352,7 @@ void dist_product_device(const double* dA_rows, i64 lda, const double* dB, i64 l
   }
   DeviceCtx& c = ctx(g_dist.device);
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c.stream;
-  const Job j = make_job(m, k, n, p, u, v, resolve_engine(flags));
+  const Job j = make_job(m, k, n, p, u, v, resolve_engine(flags), (flags & FPMM_B200_DMMA_EXACT_WORDS) != 0);
   i64 r0 = 0, rn = 0;
   dist_rows(m, g_dist.nranks, g_dist.rank, u, v, &r0, &rn);
   Workspace& ws = c.ws_for(s);

@@ -82,7 +82,8 @@ def test_every_word_pair_config(u, v):
             A = rng.integers(0, p, size=(m, k)).astype(np.float64)
             B = rng.integers(0, p, size=(k, n)).astype(np.float64)
             lam = ref_lambda(u, v, p, k)
-            C = F.mw_product(A, B, u, v, lam, F.FpContext.make(p))
+            # exactly these words on the FP64 engine: every (u,v) kernel instantiation runs
+            C = F.mw_product(A, B, u, v, lam, F.FpContext.make(p), flags=F.DMMA_EXACT_WORDS)
             assert (C == O.exact_mod_gemm(A, B, p)).all(), (u, v, bits, m, k, n)
 
 
@@ -95,9 +96,10 @@ def test_worst_case_all_p_minus_1(bits, u, v):
     for fill in (p - 1, (p - 1) // 2, (p + 1) // 2):
         A = np.full((m, k), float(fill))
         B = np.full((k, n), float(fill))
-        C = F.mw_product(A, B, u, v, ref_lambda(u, v, p, k), F.FpContext.make(p))
         want = (fill * fill * k) % p
-        assert (C == want).all(), (bits, fill)
+        for fl in (0, F.DMMA_EXACT_WORDS):  # the engine's own word choice and exactly (u,v)
+            C = F.mw_product(A, B, u, v, ref_lambda(u, v, p, k), F.FpContext.make(p), flags=fl)
+            assert (C == want).all(), (bits, fill, fl)
 
 
 def test_edge_shapes_and_values():
@@ -289,3 +291,23 @@ def test_unbalanced_preset_full_size():
     A, B, Cm = dA.cpu().numpy(), dB.cpu().numpy(), dC.cpu().numpy()
     assert O.freivalds(A, B, Cm, p, trials=2) == 0
     pa.close()
+
+
+@pytest.mark.parametrize("bits,u,v,words", [(52, 2, 2, 6), (39, 1, 3, 4), (35, 1, 2, 3), (50, 2, 2, 4)])
+def test_dmma_word_choice_at_lambda_collapse(engine, bits, u, v, words):
+    """At the rule's lambda-collapse points the FP64 engine runs cheaper word
+    counts (same C); DMMA_EXACT_WORDS keeps the caller's."""
+    if engine != "dmma":
+        pytest.skip("FP64 engine only")
+    p = F.prev_prime(1 << bits)
+    rng = np.random.default_rng(bits)
+    A = rng.integers(0, p, size=(200, 300)).astype(np.float64)
+    B = rng.integers(0, p, size=(300, 150)).astype(np.float64)
+    want = O.exact_mod_gemm(A, B, p)
+    lam = ref_lambda(u, v, p, 300)
+    tm = F.Timing()
+    assert (F.mw_product(A, B, u, v, lam, F.FpContext.make(p), timing=tm) == want).all()
+    assert tm.engine == F.ENGINE_DMMA and tm.words == words
+    tm = F.Timing()
+    assert (F.mw_product(A, B, u, v, lam, F.FpContext.make(p), flags=F.DMMA_EXACT_WORDS, timing=tm) == want).all()
+    assert tm.words == u * v

@@ -130,3 +130,28 @@ def test_rns_matches_other_engines():
     outs = [F.mw_product(A, B, pl.u, pl.v, pl.lambda_, F.FpContext.make(p), flags=e)
             for e in (F.ENGINE_RNS, F.ENGINE_I8, F.ENGINE_DMMA)]
     assert (outs[0] == outs[1]).all() and (outs[0] == outs[2]).all()
+
+
+def test_concurrent_products_on_two_streams():
+    """Products issued asynchronously on different streams get separate
+    device workspaces (packed words, residue blocks): both results exact."""
+    import torch
+    rng = np.random.default_rng(21)
+    runs = []
+    for bits, eng in ((52, F.ENGINE_RNS), (44, F.ENGINE_RNS), (30, F.ENGINE_I8)):
+        p = F.prev_prime(1 << bits)
+        A = rng.integers(0, p, size=(700, 1500)).astype(np.float64)
+        B = rng.integers(0, p, size=(1500, 600)).astype(np.float64)
+        runs.append((p, A, B, eng))
+    streams = [torch.cuda.Stream() for _ in runs]
+    outs = []
+    for (p, A, B, eng), s in zip(runs, streams):
+        dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+        dC = torch.empty((A.shape[0], B.shape[1]), dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        pl = F.plan_for_modulus(p, *A.shape, B.shape[1])
+        F.mw_product_device(dA, dB, dC, p, pl.u, pl.v, pl.lambda_, stream=s, flags=eng | F.ASYNC)
+        outs.append((dA, dB, dC))
+    torch.cuda.synchronize()
+    for (p, A, B, _), (_, _, dC) in zip(runs, outs):
+        assert (dC.cpu().numpy() == O.exact_mod_gemm(A, B, p)).all()
