@@ -648,7 +648,16 @@ int launch_gemm_rns(const Job& j, const void* apack, const void* bpack, double* 
   cp.n = j.n;
   cp.MB = q.MB, cp.NB = q.NB, cp.splits = splits, cp.group = q.group;
   const i64 tiles = static_cast<i64>(q.MB) * q.NB;
-  rns::rns_crt_kernel<<<static_cast<unsigned>(2 * tiles), 256, 0, s>>>(cp);
+  const int wpl = std::max(1, (bitsize(j.p - 1) + 7) / 8);
+  switch (wpl) {
+    case 1: rns::rns_crt_kernel<1><<<static_cast<unsigned>(2 * tiles), 256, 0, s>>>(cp); break;
+    case 2: rns::rns_crt_kernel<2><<<static_cast<unsigned>(2 * tiles), 256, 0, s>>>(cp); break;
+    case 3: rns::rns_crt_kernel<3><<<static_cast<unsigned>(2 * tiles), 256, 0, s>>>(cp); break;
+    case 4: rns::rns_crt_kernel<4><<<static_cast<unsigned>(2 * tiles), 256, 0, s>>>(cp); break;
+    case 5: rns::rns_crt_kernel<5><<<static_cast<unsigned>(2 * tiles), 256, 0, s>>>(cp); break;
+    case 6: rns::rns_crt_kernel<6><<<static_cast<unsigned>(2 * tiles), 256, 0, s>>>(cp); break;
+    default: rns::rns_crt_kernel<7><<<static_cast<unsigned>(2 * tiles), 256, 0, s>>>(cp); break;
+  }
   CUDA_OK(cudaGetLastError());
   return 2;
 }

@@ -301,105 +301,120 @@ struct CrtParams {
   uint32_t wb[kCrtGroups][kCrtPlanes];  // byte b of W_i (b < 7) / g_i (b >= 7) for the group's 4 moduli
 };
 
-// CRT of one thread's 128 columns, four per step.  All n residue words of a
-// step are loaded before any is used (n independent loads in flight per
-// thread); SPLIT: the slices' residues are summed first.
+// The n residue words of 4-column step c (SPLIT: the slices' residues summed mod m_i).
 template <bool SPLIT>
-__device__ __forceinline__ void crt_row(const CrtParams& P, const uint8_t* __restrict__ pthr, i64 slice_stride,
-                                        i64 colh, double* __restrict__ dst_row) {
-  const unsigned long long p = P.p;
-  const int ngroups = (P.nmod + 3) / 4;
-#pragma unroll 1
-  for (int c = 0; c < (kNT / 2) / 4; ++c) {
-    const i64 col0 = colh + c * 4;
-    if (col0 >= P.n) break;
-    const uint8_t* pc = pthr + (c >> 2) * (16 * kBM) + (c & 3) * 4;
-    uint32_t rw[kMaxMod];
+__device__ __forceinline__ void crt_load(const CrtParams& P, const uint8_t* __restrict__ pthr, i64 slice_stride, int c,
+                                         uint32_t (&rw)[kMaxMod]) {
+  const uint8_t* pc = pthr + (c >> 2) * (16 * kBM) + (c & 3) * 4;
 #pragma unroll
-    for (int i = 0; i < kMaxMod; ++i) {
-      if (i >= P.nmod) {
-        rw[i] = 0;
-      } else if (!SPLIT) {
-        rw[i] = __ldg(reinterpret_cast<const uint32_t*>(pc + i * kSlotPerMod));
-      } else {
-        uint32_t r = *reinterpret_cast<const uint32_t*>(pc + i * kSlotPerMod);
-        for (int s = 1; s < P.splits; ++s) {  // add the other slices' residues mod m_i
-          const uint32_t o = *reinterpret_cast<const uint32_t*>(pc + s * slice_stride + i * kSlotPerMod);
-          uint32_t out = 0;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            uint32_t v = ((r >> (8 * e)) & 0xFFu) + ((o >> (8 * e)) & 0xFFu);
-            v = v >= P.mod[i] ? v - P.mod[i] : v;
-            out |= v << (8 * e);
-          }
-          r = out;
-        }
-        rw[i] = r;
-      }
-    }
-    uint32_t acc[4][kCrtPlanes];
-#pragma unroll
-    for (int e = 0; e < 4; ++e)
-#pragma unroll
-      for (int b = 0; b < kCrtPlanes; ++b) acc[e][b] = 0;
-#pragma unroll
-    for (int gi = 0; gi < kCrtGroups; ++gi) {
-      if (gi >= ngroups) break;
-      // transpose: t[e] = the four moduli's residues of column e
-      const uint32_t a0 = rw[4 * gi], a1 = rw[4 * gi + 1], a2 = rw[4 * gi + 2], a3 = rw[4 * gi + 3];
-      const uint32_t u0 = __byte_perm(a0, a1, 0x5140), u1 = __byte_perm(a0, a1, 0x7362);
-      const uint32_t u2 = __byte_perm(a2, a3, 0x5140), u3 = __byte_perm(a2, a3, 0x7362);
-      const uint32_t t[4] = {__byte_perm(u0, u2, 0x5410), __byte_perm(u0, u2, 0x7632), __byte_perm(u1, u3, 0x5410),
-                             __byte_perm(u1, u3, 0x7632)};
-#pragma unroll
-      for (int b = 0; b < kCrtPlanes; ++b) {
-        const uint32_t wb = P.wb[gi][b];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) acc[e][b] = __dp4a(t[e], wb, acc[e][b]);
-      }
-    }
-    double out[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const uint32_t* a = acc[e];
-      // t = round(F / 2^19), F = a7 + 2^8 a8 + 2^16 a9: with u = a8 + 2^8 a9 + (a7 >> 8),
-      // F = 2^8 u + (a7 & 255) and t = (u + 2^10) >> 11 exactly (32-bit)
-      const uint32_t tt = (a[8] + (a[9] << 8) + (a[7] >> 8) + 1024u) >> 11;
-      // S = sum_i r_i W_i = sum_b 2^(8b) a_b (b < 7)
-      unsigned long long sm;
-      if (P.nmod <= 16) {  // S < 16 * 255 * 2^52 < 2^64: one u64 and one Barrett
-        const unsigned long long S = a[0] + (static_cast<unsigned long long>(a[1]) << 8) +
-                                     (static_cast<unsigned long long>(a[2]) << 16) +
-                                     (static_cast<unsigned long long>(a[3]) << 24) +
-                                     (static_cast<unsigned long long>(a[4]) << 32) +
-                                     (static_cast<unsigned long long>(a[5]) << 40) +
-                                     (static_cast<unsigned long long>(a[6]) << 48);
-        sm = barrett(S, p, P.mu);
-      } else {
-        const unsigned long long lo = a[0] + (static_cast<unsigned long long>(a[1]) << 8) +
-                                      (static_cast<unsigned long long>(a[2]) << 16) +
-                                      (static_cast<unsigned long long>(a[3]) << 24);  // < 2^45
-        const unsigned long long hi = a[4] + (static_cast<unsigned long long>(a[5]) << 8) +
-                                      (static_cast<unsigned long long>(a[6]) << 16);  // < 2^37
-        sm = barrett(dev::shoup_mulmod(hi, P.two32, P.two32_sh, p) + lo, p, P.mu);
-      }
-      // t M mod p: for n <= 16, t < 2^12 and t (M mod p) < 2^64 is one u64
-      const unsigned long long tmod = P.nmod <= 16 ? barrett(static_cast<unsigned long long>(tt) * P.Mp, p, P.mu)
-                                                   : dev::shoup_mulmod(tt, P.Mp, P.Mp_sh, p);
-      const unsigned long long r = sm >= tmod ? sm - tmod : sm + p - tmod;
-      out[e] = __longlong_as_double(static_cast<long long>(r | 0x4330000000000000ull)) - 4503599627370496.0;
-    }
-    double* dst = dst_row + c * 4;
-    if (col0 + 4 <= P.n && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-      *reinterpret_cast<double2*>(dst) = make_double2(out[0], out[1]);
-      *reinterpret_cast<double2*>(dst + 2) = make_double2(out[2], out[3]);
+  for (int i = 0; i < kMaxMod; ++i) {
+    if (i >= P.nmod) {
+      rw[i] = 0;
+    } else if (!SPLIT) {
+      rw[i] = __ldg(reinterpret_cast<const uint32_t*>(pc + i * kSlotPerMod));
     } else {
-      for (int e = 0; e < 4 && col0 + e < P.n; ++e) dst[e] = out[e];
+      uint32_t r = *reinterpret_cast<const uint32_t*>(pc + i * kSlotPerMod);
+      for (int s = 1; s < P.splits; ++s) {  // add the other slices' residues mod m_i
+        const uint32_t o = *reinterpret_cast<const uint32_t*>(pc + s * slice_stride + i * kSlotPerMod);
+        uint32_t out = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          uint32_t v = ((r >> (8 * e)) & 0xFFu) + ((o >> (8 * e)) & 0xFFu);
+          v = v >= P.mod[i] ? v - P.mod[i] : v;
+          out |= v << (8 * e);
+        }
+        r = out;
+      }
+      rw[i] = r;
     }
   }
 }
 
-// One block of 256 threads per (pair tile, CTA rank): thread = (column half, row).
+// CRT of the 4 columns of step c from their residue words -> C.
+template <int WPL>
+__device__ __forceinline__ void crt_step(const CrtParams& P, int c, i64 colh, double* __restrict__ dst_row,
+                                         const uint32_t (&rw)[kMaxMod]) {
+  const i64 col0 = colh + c * 4;
+  if (col0 >= P.n) return;
+  const unsigned long long p = P.p;
+  const int ngroups = (P.nmod + 3) / 4;
+  uint32_t acc[4][kCrtPlanes];
+#pragma unroll
+  for (int e = 0; e < 4; ++e)
+#pragma unroll
+    for (int b = 0; b < kCrtPlanes; ++b) acc[e][b] = 0;  // planes WPL..6 stay zero
+#pragma unroll
+  for (int gi = 0; gi < kCrtGroups; ++gi) {
+    if (gi >= ngroups) break;
+    // transpose: t[e] = the four moduli's residues of column e
+    const uint32_t a0 = rw[4 * gi], a1 = rw[4 * gi + 1], a2 = rw[4 * gi + 2], a3 = rw[4 * gi + 3];
+    const uint32_t u0 = __byte_perm(a0, a1, 0x5140), u1 = __byte_perm(a0, a1, 0x7362);
+    const uint32_t u2 = __byte_perm(a2, a3, 0x5140), u3 = __byte_perm(a2, a3, 0x7362);
+    const uint32_t t[4] = {__byte_perm(u0, u2, 0x5410), __byte_perm(u0, u2, 0x7632), __byte_perm(u1, u3, 0x5410),
+                           __byte_perm(u1, u3, 0x7632)};
+#pragma unroll
+    for (int b = 0; b < kCrtPlanes; ++b) {
+      if (b >= WPL && b < 7) continue;  // W_i < p < 2^(8 WPL): planes WPL..6 are zero
+      const uint32_t wb = P.wb[gi][b];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[e][b] = __dp4a(t[e], wb, acc[e][b]);
+    }
+  }
+  double out[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const uint32_t* a = acc[e];
+    // t = round(F / 2^19), F = a7 + 2^8 a8 + 2^16 a9: with u = a8 + 2^8 a9 + (a7 >> 8),
+    // F = 2^8 u + (a7 & 255) and t = (u + 2^10) >> 11 exactly (32-bit)
+    const uint32_t tt = (a[8] + (a[9] << 8) + (a[7] >> 8) + 1024u) >> 11;
+    // S = sum_i r_i W_i = sum_b 2^(8b) a_b (b < WPL)
+    unsigned long long sm;
+    if (P.nmod <= 16) {  // S < 16 * 255 * 2^52 < 2^64: one u64 and one Barrett
+      unsigned long long S = 0;
+#pragma unroll
+      for (int b = 0; b < WPL; ++b) S += static_cast<unsigned long long>(a[b]) << (8 * b);
+      sm = barrett(S, p, P.mu);
+    } else {
+      const unsigned long long lo = a[0] + (static_cast<unsigned long long>(a[1]) << 8) +
+                                    (static_cast<unsigned long long>(a[2]) << 16) +
+                                    (static_cast<unsigned long long>(a[3]) << 24);  // < 2^45
+      const unsigned long long hi = a[4] + (static_cast<unsigned long long>(a[5]) << 8) +
+                                    (static_cast<unsigned long long>(a[6]) << 16);  // < 2^37
+      sm = barrett(dev::shoup_mulmod(hi, P.two32, P.two32_sh, p) + lo, p, P.mu);
+    }
+    // t M mod p: for n <= 16, t < 2^12 and t (M mod p) < 2^64 is one u64
+    const unsigned long long tmod = P.nmod <= 16 ? barrett(static_cast<unsigned long long>(tt) * P.Mp, p, P.mu)
+                                                 : dev::shoup_mulmod(tt, P.Mp, P.Mp_sh, p);
+    const unsigned long long r = sm >= tmod ? sm - tmod : sm + p - tmod;
+    out[e] = __longlong_as_double(static_cast<long long>(r | 0x4330000000000000ull)) - 4503599627370496.0;
+  }
+  double* dst = dst_row + c * 4;
+  if (col0 + 4 <= P.n && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+    *reinterpret_cast<double2*>(dst) = make_double2(out[0], out[1]);
+    *reinterpret_cast<double2*>(dst + 2) = make_double2(out[2], out[3]);
+  } else {
+    for (int e = 0; e < 4 && col0 + e < P.n; ++e) dst[e] = out[e];
+  }
+}
+
+// CRT of one thread's 128 columns, four per step; all n residue words of a
+// step are loaded before any is used.  (Pipelining the next step's loads
+// measured 15-20% slower: the extra registers cost a resident block per SM.)
+template <int WPL, bool SPLIT>
+__device__ __forceinline__ void crt_row(const CrtParams& P, const uint8_t* __restrict__ pthr, i64 slice_stride,
+                                        i64 colh, double* __restrict__ dst_row) {
+  constexpr int kSteps = (kNT / 2) / 4;
+#pragma unroll 1
+  for (int c = 0; c < kSteps; ++c) {
+    if (colh + c * 4 >= P.n) break;
+    uint32_t rw[kMaxMod];
+    crt_load<SPLIT>(P, pthr, slice_stride, c, rw);
+    crt_step<WPL>(P, c, colh, dst_row, rw);
+  }
+}
+
+// WPL = byte planes of W_i (ceil(bits(p - 1) / 8)): the kernel skips the zero planes.
+template <int WPL>
 __global__ void __launch_bounds__(256) rns_crt_kernel(const __grid_constant__ CrtParams P) {
   const int tile = blockIdx.x >> 1, rank = blockIdx.x & 1;
   const int row_in_tile = threadIdx.x % kBM, half = threadIdx.x / kBM;
@@ -416,8 +431,8 @@ __global__ void __launch_bounds__(256) rns_crt_kernel(const __grid_constant__ Cr
                         (static_cast<i64>(half) * 8 * kBM + row_in_tile) * 16;
   const i64 slice_stride = tiles * 2 * P.nmod * kSlotPerMod;
   double* dst_row = P.C + row * P.ldc + colh;
-  if (P.splits == 1) crt_row<false>(P, pthr, slice_stride, colh, dst_row);
-  else crt_row<true>(P, pthr, slice_stride, colh, dst_row);
+  if (P.splits == 1) crt_row<WPL, false>(P, pthr, slice_stride, colh, dst_row);
+  else crt_row<WPL, true>(P, pthr, slice_stride, colh, dst_row);
 }
 
 // ---- CTA-pair plumbing ----
