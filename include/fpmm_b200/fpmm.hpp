@@ -10,8 +10,10 @@
 // Differences, by design:
 //   * only T = double (FpContext<float> / t = 24 is out of scope);
 //   * GemmKernel selection is accepted for signature parity; every product
-//     runs the fused multiword kernel.  kernel_by_name("b200") returns the
-//     panel-level kernel (DMMA, exact C += A B) for plugin-style callers.
+//     runs a fused engine.  kernel_by_name("b200") (alias "accelerated")
+//     selects the library default; "b200-rns", "b200-i8" and "b200-dmma" pin
+//     an engine (FPMM_B200_ENGINE_*).  Each also is the panel-level kernel
+//     (DMMA, exact C += A B) for plugin-style callers.
 #pragma once
 
 #include <cstdint>
@@ -185,23 +187,43 @@ class GemmKernel {
 
 class B200Kernel final : public GemmKernel<double> {
  public:
+  constexpr B200Kernel(std::string_view name, unsigned engine) : name_(name), engine_(engine) {}
   void accumulate(MatView<double> c, ConstMatView<double> a, ConstMatView<double> b) const override {
     if (a.rows != c.rows || b.cols != c.cols || a.cols != b.rows) throw Error("accumulate: dimension mismatch");
     detail::check(fpmm_b200_accumulate(c.data, c.stride, a.data, a.stride, b.data, b.stride, c.rows, a.cols, c.cols));
   }
-  std::string_view name() const override { return "b200"; }
+  std::string_view name() const override { return name_; }
+  unsigned engine() const { return engine_; }  // FPMM_B200_ENGINE_* flag, 0 = library default
+
+ private:
+  std::string_view name_;
+  unsigned engine_;
 };
 
 template <typename T>
 const GemmKernel<T>& b200_kernel() {
-  static const B200Kernel k;
+  static const B200Kernel k("b200", 0u);
   return k;
 }
 template <typename T>
 const GemmKernel<T>* kernel_by_name(std::string_view name) {
+  static const B200Kernel rns("b200-rns", FPMM_B200_ENGINE_RNS), i8("b200-i8", FPMM_B200_ENGINE_I8),
+      dmma("b200-dmma", FPMM_B200_ENGINE_DMMA);
   if (name == "b200" || name == "accelerated") return &b200_kernel<T>();
+  if (name == "b200-rns") return &rns;
+  if (name == "b200-i8") return &i8;
+  if (name == "b200-dmma") return &dmma;
   return nullptr;
 }
+
+namespace detail {
+// engine flag carried by the caller's kernel choice (0 for foreign kernels: the default)
+template <typename T>
+unsigned engine_of(const GemmKernel<T>& k) {
+  const auto* b = dynamic_cast<const B200Kernel*>(&k);
+  return b ? b->engine() : 0u;
+}
+}  // namespace detail
 
 // multiword.hpp:12-24
 inline u64 word_base(u64 p, int u) {
@@ -257,10 +279,10 @@ void block_gemm_mod(Mat<T>& C, const Mat<T>& A, const Mat<T>& B, u64 lambda, con
 namespace detail {
 template <typename T>
 Mat<T> product(const Mat<T>& A, const Mat<T>& B, int u, int v, u64 lambda, const FpContext<T>& F, int variant,
-               int ngpus) {
+               int ngpus, unsigned engine = 0) {
   if (A.cols() != B.rows()) throw Error("multiword product: dimension mismatch");
   Mat<T> C(A.rows(), B.cols());
-  const unsigned flags = F.prime() ? 0u : FPMM_B200_ALLOW_COMPOSITE;
+  const unsigned flags = (F.prime() ? 0u : FPMM_B200_ALLOW_COMPOSITE) | engine;
   check(fpmm_b200_mw_product(A.data(), A.cols(), B.data(), B.cols(), C.data(), C.cols(), A.rows(), A.cols(),
                              B.cols(), F.p(), u, v, lambda, variant, ngpus, flags, nullptr));
   C.set_max_hint(F.p() - 1);
@@ -269,7 +291,7 @@ Mat<T> product(const Mat<T>& A, const Mat<T>& B, int u, int v, u64 lambda, const
 
 template <typename T>
 Mat<T> words_product(const WordDecomposition<T>& da, const WordDecomposition<T>& db, index_t m, index_t k,
-                     index_t n, u64 lambda, const FpContext<T>& F, int variant) {
+                     index_t n, u64 lambda, const FpContext<T>& F, int variant, unsigned engine = 0) {
   const int u = da.word_count(), v = db.word_count();
   if (u < 1 || v < 1) throw Error("multiword product: word counts must be positive");
   std::vector<T> aw(static_cast<size_t>(u) * m * k), bw(static_cast<size_t>(v) * k * n);
@@ -282,7 +304,7 @@ Mat<T> words_product(const WordDecomposition<T>& da, const WordDecomposition<T>&
     std::copy(db.words[j].data(), db.words[j].data() + k * n, bw.data() + static_cast<i64>(j) * k * n);
   }
   Mat<T> C(m, n);
-  const unsigned flags = F.prime() ? 0u : FPMM_B200_ALLOW_COMPOSITE;
+  const unsigned flags = (F.prime() ? 0u : FPMM_B200_ALLOW_COMPOSITE) | engine;
   check(fpmm_b200_mw_product_words(aw.data(), m * k, k > 0 ? k : 1, da.base, u, bw.data(), k * n, n > 0 ? n : 1,
                                    db.base, v, C.data(), n > 0 ? n : 1, m, k, n, F.p(), lambda, variant, flags,
                                    nullptr));
@@ -294,13 +316,13 @@ Mat<T> words_product(const WordDecomposition<T>& da, const WordDecomposition<T>&
 // multiword.hpp:113-139
 template <typename T>
 Mat<T> mw_product_words(const WordDecomposition<T>& da, const WordDecomposition<T>& db, index_t m, index_t k,
-                        index_t n, u64 lambda, const FpContext<T>& F, const GemmKernel<T>& = b200_kernel<T>()) {
-  return detail::words_product(da, db, m, k, n, lambda, F, FPMM_B200_PLAIN);
+                        index_t n, u64 lambda, const FpContext<T>& F, const GemmKernel<T>& kernel = b200_kernel<T>()) {
+  return detail::words_product(da, db, m, k, n, lambda, F, FPMM_B200_PLAIN, detail::engine_of(kernel));
 }
 template <typename T>
 Mat<T> mw_product(const Mat<T>& A, const Mat<T>& B, int u, int v, u64 lambda, const FpContext<T>& F,
-                  const GemmKernel<T>& = b200_kernel<T>()) {
-  return detail::product(A, B, u, v, lambda, F, FPMM_B200_PLAIN, 1);
+                  const GemmKernel<T>& kernel = b200_kernel<T>()) {
+  return detail::product(A, B, u, v, lambda, F, FPMM_B200_PLAIN, 1, detail::engine_of(kernel));
 }
 // row-sharded over devices 0..ngpus-1 of this process (NCCL broadcast of B words)
 template <typename T>
@@ -319,25 +341,25 @@ inline u64 concat_workspace_entries(int u, int v, index_t m, index_t n, ConcatSi
 template <typename T>
 Mat<T> mw_product_concat_words(const WordDecomposition<T>& da, const WordDecomposition<T>& db, index_t m,
                                index_t k, index_t n, u64 lambda, const FpContext<T>& F,
-                               const GemmKernel<T>& = b200_kernel<T>(), ConcatSide = ConcatSide::auto_pick) {
-  return detail::words_product(da, db, m, k, n, lambda, F, FPMM_B200_CONCAT);
+                               const GemmKernel<T>& kernel = b200_kernel<T>(), ConcatSide = ConcatSide::auto_pick) {
+  return detail::words_product(da, db, m, k, n, lambda, F, FPMM_B200_CONCAT, detail::engine_of(kernel));
 }
 template <typename T>
 Mat<T> mw_product_concat(const Mat<T>& A, const Mat<T>& B, int u, int v, u64 lambda, const FpContext<T>& F,
-                         const GemmKernel<T>& = b200_kernel<T>(), ConcatSide = ConcatSide::auto_pick) {
-  return detail::product(A, B, u, v, lambda, F, FPMM_B200_CONCAT, 1);
+                         const GemmKernel<T>& kernel = b200_kernel<T>(), ConcatSide = ConcatSide::auto_pick) {
+  return detail::product(A, B, u, v, lambda, F, FPMM_B200_CONCAT, 1, detail::engine_of(kernel));
 }
 // multiword.hpp:222-254 (inverse-free; composite p allowed)
 template <typename T>
 Mat<T> mw_product_workspace_words(const WordDecomposition<T>& da, const WordDecomposition<T>& db, index_t m,
                                   index_t k, index_t n, u64 lambda, const FpContext<T>& F,
-                                  const GemmKernel<T>& = b200_kernel<T>()) {
-  return detail::words_product(da, db, m, k, n, lambda, F, FPMM_B200_WORKSPACE);
+                                  const GemmKernel<T>& kernel = b200_kernel<T>()) {
+  return detail::words_product(da, db, m, k, n, lambda, F, FPMM_B200_WORKSPACE, detail::engine_of(kernel));
 }
 template <typename T>
 Mat<T> mw_product_workspace(const Mat<T>& A, const Mat<T>& B, int u, int v, u64 lambda, const FpContext<T>& F,
-                            const GemmKernel<T>& = b200_kernel<T>()) {
-  return detail::product(A, B, u, v, lambda, F, FPMM_B200_WORKSPACE, 1);
+                            const GemmKernel<T>& kernel = b200_kernel<T>()) {
+  return detail::product(A, B, u, v, lambda, F, FPMM_B200_WORKSPACE, 1, detail::engine_of(kernel));
 }
 
 // planner.hpp:12-102

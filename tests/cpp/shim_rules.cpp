@@ -41,6 +41,16 @@ int main() {
     threw = true;
   }
   REQUIRE(threw);
+  // kernel names pin an engine (plugin conformance: name() round-trips)
+  REQUIRE(kernel_by_name<double>("b200") == &b200_kernel<double>());
+  REQUIRE(kernel_by_name<double>("accelerated") == &b200_kernel<double>());
+  for (const char* nm : {"b200-rns", "b200-i8", "b200-dmma"}) {
+    const GemmKernel<double>* k = kernel_by_name<double>(nm);
+    REQUIRE(k && k->name() == nm);
+  }
+  REQUIRE(detail::engine_of(*kernel_by_name<double>("b200-rns")) == FPMM_B200_ENGINE_RNS);
+  REQUIRE(detail::engine_of(b200_kernel<double>()) == 0u);
+  REQUIRE(kernel_by_name<double>("naive") == nullptr);
   auto M = random_mat<double>(3, 4, 31, 1);
   REQUIRE(M.max_bound() <= 30);
   std::printf("OK\n");
