@@ -594,8 +594,8 @@ CUtensorMap chunk_map(const void* base, size_t bytes) {
   return m;
 }
 
-int launch_gemm_rns(const Job& j, const void* apack, const void* bpack, double* C, i64 ldc, i64 rows,
-                    cudaStream_t s, cudaEvent_t mid, Workspace& ws) {
+int launch_gemm_rns_rows(const Job& j, const void* apack, const void* bpack, double* C, i64 ldc, i64 rows,
+                         cudaStream_t s, cudaEvent_t mid, Workspace& ws) {
   rns::Params q = j.rp;
   q.apack = static_cast<const uint8_t*>(apack);
   q.bpack = static_cast<const uint8_t*>(bpack);
@@ -660,6 +660,29 @@ int launch_gemm_rns(const Job& j, const void* apack, const void* bpack, double* 
   }
   CUDA_OK(cudaGetLastError());
   return 2;
+}
+
+// The parked residues take n bytes per output element (and split-K slice);
+// above kRnsResidueBudget the product runs in row blocks of whole pair tiles
+// that reuse one residue buffer (e.g. 65536^2 outputs at n = 11: 47 GB).
+constexpr size_t kRnsResidueBudget = size_t{8} << 30;
+int launch_gemm_rns(const Job& j, const void* apack, const void* bpack, double* C, i64 ldc, i64 rows,
+                    cudaStream_t s, cudaEvent_t mid, Workspace& ws) {
+  const i64 pair_rows = (rows + rns::kPairM - 1) / rns::kPairM;
+  const size_t per_pair_row = static_cast<size_t>(j.NB) * 2 * j.nmod * rns::kSlotPerMod *
+                              std::max<i64>(1, (j.KB + j.rp.seg_kb - 1) / j.rp.seg_kb);
+  size_t budget = kRnsResidueBudget;
+  if (const char* e = std::getenv("FPMM_B200_RNS_RESIDUE_BUDGET")) budget = std::strtoull(e, nullptr, 10);
+  const i64 chunk = std::max<i64>(1, static_cast<i64>(budget / per_pair_row));
+  if (pair_rows <= chunk) return launch_gemm_rns_rows(j, apack, bpack, C, ldc, rows, s, mid, ws);
+  int launches = 0;
+  for (i64 pr = 0; pr < pair_rows; pr += chunk) {
+    const i64 r0 = pr * rns::kPairM, rn = std::min<i64>(rows - r0, chunk * rns::kPairM);
+    launches += launch_gemm_rns_rows(j, static_cast<const uint8_t*>(apack) + pr * j.per_rb_bytes, bpack,
+                                     C + r0 * ldc, ldc, rn, s, nullptr, ws);
+  }
+  if (mid) CUDA_OK(cudaEventRecord(mid, s));  // row blocks interleave GEMM and CRT: all counted as GEMM
+  return launches;
 }
 
 // Launches the product kernel(s) for packed operands; returns the launch count.

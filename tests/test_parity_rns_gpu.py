@@ -155,3 +155,17 @@ def test_concurrent_products_on_two_streams():
     torch.cuda.synchronize()
     for (p, A, B, _), (_, _, dC) in zip(runs, outs):
         assert (dC.cpu().numpy() == O.exact_mod_gemm(A, B, p)).all()
+
+
+def test_rns_row_blocks_under_a_residue_budget(monkeypatch):
+    """A product whose parked residues exceed the budget runs in row blocks of
+    pair tiles (here forced with a tiny budget): same C."""
+    monkeypatch.setenv("FPMM_B200_RNS_RESIDUE_BUDGET", str(1 << 20))
+    p = F.prev_prime(1 << 50)
+    rng = np.random.default_rng(8)
+    A = rng.integers(0, p, size=(1100, 700)).astype(np.float64)
+    B = rng.integers(0, p, size=(700, 900)).astype(np.float64)
+    tm = F.Timing()
+    C = F.mw_product(A, B, 2, 2, 7, F.FpContext.make(p), flags=RNS, timing=tm)
+    assert (C == O.exact_mod_gemm(A, B, p)).all()
+    assert tm.launches > 4  # several GEMM + CRT pairs
