@@ -3,7 +3,8 @@
 
   python -m paper_2601_07508_b200.cli bench [--scenario square|unbalanced] [--dims m,k,n]
         [--scale S] [--bits 20 26 ...] [--variant u,v|auto ...] [--lambda auto|N]
-        [--kernel b200|b200-i8|b200-dmma] [--runs R] [--seed S] [--out CSV] [--extended]
+        [--kernel b200|b200-rns|b200-i8|b200-dmma|b200-dmma-exact] [--runs R] [--seed S] [--out CSV]
+        [--extended] [--device-resident]
   python -m paper_2601_07508_b200.cli crossover bench.csv [--out CSV]
   python -m paper_2601_07508_b200.cli plan --bits B [--dims m,k,n] [--min-lambda L]
 
@@ -27,7 +28,7 @@ import time
 
 import numpy as np
 
-from . import (ENGINE_DMMA, ENGINE_I8, ENGINE_RNS, Error, FpContext, InfeasibleError, Timing, kVariants,
+from . import (DMMA_EXACT_WORDS, ENGINE_DMMA, ENGINE_I8, ENGINE_RNS, Error, FpContext, InfeasibleError, Timing, kVariants,
                matrix_seed, mw_block_size, plan_for_modulus, prev_prime, random_mat,
                variant_admits_bits)
 
@@ -35,7 +36,9 @@ SCHEMA_VERSION = 1
 HEADER = ["schema_version", "scenario", "m", "k", "n", "bits", "p", "u", "v", "concat", "lambda",
           "kernel", "runs", "t_avg_s", "eff_gflops", "status"]
 EXTENDED = ["engine", "lambda_k", "gpus", "device_ms"]
-KERNELS = {"b200": 0, "b200-i8": ENGINE_I8, "b200-rns": ENGINE_RNS, "b200-dmma": ENGINE_DMMA}
+KERNELS = {"b200": 0, "b200-i8": ENGINE_I8, "b200-rns": ENGINE_RNS, "b200-dmma": ENGINE_DMMA,
+           # the FP64 engine with exactly the variant's (u,v) words: per-variant timings for crossover
+           "b200-dmma-exact": ENGINE_DMMA | DMMA_EXACT_WORDS}
 
 
 def preset_dims(scenario: str, scale: float):
@@ -102,6 +105,11 @@ def run_bench(args) -> list:
                 B = random_mat(k, n, p, matrix_seed(args.seed, bits, m, k, n, 0xB))
                 Cm = np.empty((m, n))
                 prepared = None
+                dev_in = None
+                if args.device_resident and args.scenario == "square":
+                    import torch
+                    dev_in = (torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(),
+                              torch.empty((m, n), dtype=torch.float64, device="cuda"))
                 if args.scenario == "unbalanced":
                     import torch
                     from . import PreparedA
@@ -118,7 +126,10 @@ def run_bench(args) -> list:
                     lam = int(args.lambda_) if args.lambda_ != "auto" else min(mw_block_size(u, v, p) or 0, k)
                     if lam < 1:
                         raise InfeasibleError("block size infeasible")
-                    if prepared is None:
+                    if dev_in is not None:
+                        from . import mw_product_device
+                        mw_product_device(dev_in[0], dev_in[1], dev_in[2], p, u, v, lam, flags=flags, timing=tm)
+                    elif prepared is None:
                         from . import mw_product
                         mw_product(A, B, u, v, lam, F, flags=flags, timing=tm, out=Cm)
                     else:
@@ -131,7 +142,8 @@ def run_bench(args) -> list:
                         dev += tm.total_ms
                     lam_used = lam
                 rec["lambda"] = lam_used
-                rec["t_avg_s"] = total / args.runs
+                # device-resident runs are timed by the library's CUDA events (no PCIe)
+                rec["t_avg_s"] = (dev / 1e3 if dev_in is not None else total) / args.runs
                 rec["eff_gflops"] = effective_gflops(m, k, n, rec["t_avg_s"])
                 rec["engine"] = ("rns" if flags & ENGINE_RNS else "dmma" if flags & ENGINE_DMMA
                                  else "i8" if flags & ENGINE_I8 else "auto")
@@ -235,6 +247,8 @@ def main(argv=None) -> int:
     b.add_argument("--seed", type=int, default=1)
     b.add_argument("--out")
     b.add_argument("--extended", action="store_true")
+    b.add_argument("--device-resident", action="store_true",
+                   help="square scenario with inputs already on the GPU, timed by CUDA events (no PCIe)")
     c = sub.add_parser("crossover", help="best-variant bitsize intervals from a bench CSV")
     c.add_argument("csv")
     c.add_argument("--out")
