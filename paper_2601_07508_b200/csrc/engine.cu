@@ -189,6 +189,7 @@ struct Job {
   int u, v;
   int engine = kDmma;
   int D = 0;  // int8 engine: base-256 digits per residue
+  bool narrow = false;  // int8 engine: NT = 32 tiles for n <= 32
   int BM = 0, BN = 0, MB = 0, NB = 0, KB = 0;
   size_t apack_bytes = 0, bpack_bytes = 0, per_rb_bytes = 0;
   i64 lambda_k = 0;
@@ -200,6 +201,21 @@ struct Job {
   rns::PackParams rpp{};
   rns::CrtParams rcp{};
 };
+
+// int8 engine kernels by digit count and tile width (wide default or NT = 32)
+template <typename F>
+void dispatch_dn(int D, bool narrow, F&& f) {
+  switch (D) {
+    case 1: return narrow ? f.template operator()<1, 32>() : f.template operator()<1, i8::kWideNT<1>>();
+    case 2: return narrow ? f.template operator()<2, 32>() : f.template operator()<2, i8::kWideNT<2>>();
+    case 3: return narrow ? f.template operator()<3, 32>() : f.template operator()<3, i8::kWideNT<3>>();
+    case 4: return narrow ? f.template operator()<4, 32>() : f.template operator()<4, i8::kWideNT<4>>();
+    case 5: return narrow ? f.template operator()<5, 32>() : f.template operator()<5, i8::kWideNT<5>>();
+    case 6: return narrow ? f.template operator()<6, 32>() : f.template operator()<6, i8::kWideNT<6>>();
+    case 7: return f.template operator()<7, 32>();
+  }
+  throw Failure(FPMM_B200_EERROR, "int8 engine: unsupported digit count " + std::to_string(D));
+}
 
 template <typename F>
 void dispatch_d(int D, F&& f) {
@@ -242,7 +258,7 @@ int auto_engine(i64 m, i64 k, i64 n, u64 p) {
     return kI8;
   }
   int nt = 32;
-  dispatch_d(D, [&]<int DD>() { nt = i8::Cfg<DD>::kNT; });
+  dispatch_d(D, [&]<int DD>() { nt = n <= 32 ? 32 : i8::kWideNT<DD>; });
   const i64 KB = (k + 63) / 64;
   // fraction of the SMs (pairs) a product keeps busy, split-K included
   auto busy = [&](i64 tiles, i64 slots) {
@@ -270,12 +286,14 @@ Job make_i8_job(i64 m, i64 k, i64 n, u64 p) {
   j.BM = i8::kBM;
   j.MB = static_cast<int>((m + i8::kBM - 1) / i8::kBM);
   j.KB = static_cast<int>((k + i8::kBK - 1) / i8::kBK);
-  dispatch_d(j.D, [&]<int D>() {
-    j.BN = i8::Cfg<D>::kNT;
+  j.narrow = n <= 32;
+  dispatch_dn(j.D, j.narrow, [&]<int D, int NT>() {
+    using CF = i8::Cfg<D, NT>;
+    j.BN = CF::kNT;
     j.NB = static_cast<int>((n + j.BN - 1) / j.BN);
-    j.per_rb_bytes = static_cast<size_t>(j.KB) * i8::Cfg<D>::kAStage;
+    j.per_rb_bytes = static_cast<size_t>(j.KB) * CF::kAStage;  // A's layout does not depend on NT
     j.apack_bytes = static_cast<size_t>(j.MB) * j.per_rb_bytes;
-    j.bpack_bytes = static_cast<size_t>(j.NB) * j.KB * i8::Cfg<D>::kBStage;
+    j.bpack_bytes = static_cast<size_t>(j.NB) * j.KB * CF::kBStage;
   });
   // exact while pairs * K_seg * 255^2 < 2^32 (weight block read as unsigned)
   const u64 terms = 0xFFFFFFFFull / (static_cast<u64>(j.D) * 255 * 255);
@@ -489,8 +507,8 @@ void launch_pack_b(const Job& j, const double* B, i64 ldb, void* bpack, int* err
     if (err && j.k > 0 && j.n > 0)
       check_residues_kernel<<<grid_for(j.k * j.n, 256), 256, 0, s>>>(B, ldb, j.k, j.n, j.p, err);
     const i64 tiles = static_cast<i64>(j.KB) * j.NB;
-    dispatch_d(j.D, [&]<int D>() {
-      i8::pack_b_i8<D><<<static_cast<unsigned>(std::min<i64>(std::max<i64>(tiles, 1), 148 * 16)), 256, 0, s>>>(
+    dispatch_dn(j.D, j.narrow, [&]<int D, int NT>() {
+      i8::pack_b_i8<D, NT><<<static_cast<unsigned>(std::min<i64>(std::max<i64>(tiles, 1), 148 * 16)), 256, 0, s>>>(
           B, ldb, j.k, j.n, j.KB, j.NB, static_cast<uint8_t*>(bpack));
     });
     CUDA_OK(cudaGetLastError());
@@ -546,9 +564,9 @@ int launch_gemm_i8(const Job& j, const void* apack, const void* bpack, double* C
   CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const i64 items = static_cast<i64>(q.MB) * q.NB * splits;
   const unsigned grid = static_cast<unsigned>(std::max<i64>(1, std::min<i64>(items, sms)));
-  dispatch_d(j.D, [&]<int D>() {
-    using CF = i8::Cfg<D>;
-    auto kern = i8::mwi8_kernel<D>;
+  dispatch_dn(j.D, j.narrow, [&]<int D, int NT>() {
+    using CF = i8::Cfg<D, NT>;
+    auto kern = i8::mwi8_kernel<D, NT>;
     static bool configured[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);

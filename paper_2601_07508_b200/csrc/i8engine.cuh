@@ -38,9 +38,12 @@ constexpr int kThreads = 192;      // 6 warps
 // (2D-1) NT <= 512 TMEM columns and N_mma = D NT <= 256, N_mma % 16 == 0.  Wider tiles read
 // less shared memory per MMA (A is re-read once per MMA) and amortise the
 // per-tile epilogue over more work.
+// A narrow B (n <= 32, e.g. the unbalanced scenario's 32 columns) uses NT = 32.
 template <int D>
+constexpr int kWideNT = D == 1 ? 256 : D == 2 ? 128 : D == 3 ? 80 : D == 4 ? 64 : D == 5 ? 48 : D == 6 ? 40 : 32;
+template <int D, int NT_ = kWideNT<D>>
 struct Cfg {
-  static constexpr int kNT = D == 1 ? 256 : D == 2 ? 128 : D == 3 ? 80 : D == 4 ? 64 : D == 5 ? 48 : D == 6 ? 40 : 32;
+  static constexpr int kNT = NT_;
   static constexpr int kAStage = D * kBM * kBK;        // bytes: D digit tiles of 128 x 64
   static constexpr int kBStage = D * kNT * kBK;        // bytes: B_cat tile of (NT D) x 64
   static constexpr int kStageBytes = kAStage + kBStage;
@@ -253,10 +256,9 @@ __global__ void __launch_bounds__(256) pack_a_i8(const double* __restrict__ A, i
 // K-major.  Chunk (cb, kb) (contiguous, kBStage bytes):
 //   [k16 c (4)][row group g (NT D / 8)][row r (8)][16 bytes]
 // A block transposes 64 (k) x 32 (col) sub-tiles through shared memory.
-template <int D>
+template <int D, int NT>
 __global__ void __launch_bounds__(256) pack_b_i8(const double* __restrict__ B, i64 ldb, i64 k, i64 n,
                                                  int KB, int NB, uint8_t* __restrict__ out) {
-  constexpr int NT = Cfg<D>::kNT;
   constexpr int SW = NT % 32 == 0 ? 32 : NT % 16 == 0 ? 16 : 8;  // sub-block columns
   constexpr int SUB = NT / SW;
   __shared__ unsigned long long tile[kBK][SW + 1];
@@ -271,7 +273,7 @@ __global__ void __launch_bounds__(256) pack_b_i8(const double* __restrict__ B, i
       tile[kr][cc] = (kk < k && col < n) ? static_cast<unsigned long long>(B[kk * ldb + col]) : 0ull;
     }
     __syncthreads();
-    uint8_t* base = out + (cb * KB + kb) * static_cast<i64>(Cfg<D>::kBStage);
+    uint8_t* base = out + (cb * KB + kb) * static_cast<i64>(Cfg<D, NT>::kBStage);
     // units: (digit j, column cc, k16 chunk q): 16 bytes each
     for (int u = threadIdx.x; u < D * SW * (kBK / 16); u += blockDim.x) {
       // lanes walk the 32 columns: 2-way (64-bit) bank access, and 32
@@ -367,9 +369,9 @@ __device__ __forceinline__ void epi_chunk(const Params& P, uint32_t trow, int c0
 // Persistent: one CTA per SM loops over work items (TMEM allocation, barrier
 // set-up and the pipeline fill are paid once per SM, and the TMA producer
 // runs ahead into the next item while the epilogue reconstructs the last).
-template <int D>
+template <int D, int NTC>
 __global__ void __launch_bounds__(kThreads, 1) mwi8_kernel(const __grid_constant__ Params P) {
-  using CF = Cfg<D>;
+  using CF = Cfg<D, NTC>;
   constexpr int S = CF::kStages, NT = CF::kNT, NB_ = CF::kBlocks;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;
