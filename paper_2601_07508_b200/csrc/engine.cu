@@ -175,6 +175,24 @@ DigitParams digit_params(u64 p, int w) {
   return d;
 }
 
+// Split-K count for `tiles` output tiles on `slots` persistent CTAs (or
+// pairs): the smallest count in [lo, hi] whose last wave is well filled, i.e.
+// maximising items / (waves * slots) with a 2% cost per extra slice.
+int pick_splits(i64 tiles, i64 slots, i64 lo, i64 hi) {
+  if (tiles <= 0) return 1;
+  hi = std::max<i64>(hi, 1);
+  lo = std::min<i64>(std::max<i64>(lo, 1), hi);
+  i64 best = lo;
+  double best_score = -1;
+  for (i64 s = lo; s <= hi; ++s) {
+    const i64 items = tiles * s;
+    const i64 waves = (items + slots - 1) / slots;
+    const double score = static_cast<double>(items) / static_cast<double>(waves * slots) - 0.02 * (s - lo);
+    if (score > best_score + 1e-9) best_score = score, best = s;
+  }
+  return static_cast<int>(best);
+}
+
 int grid_for(i64 items, int threads) {
   const i64 blocks = (items + threads - 1) / threads;
   return static_cast<int>(std::min<i64>(std::max<i64>(blocks, 1), 148 * 64));
@@ -540,7 +558,7 @@ int launch_gemm_i8(const Job& j, const void* apack, const void* bpack, double* C
   int splits = 1;
   if (tiles0 > 0 && tiles0 < 2 * 148) {
     const i64 want = (2 * 148 + tiles0 - 1) / tiles0;
-    splits = static_cast<int>(std::max<i64>(1, std::min<i64>({want, j.KB / 16, 32})));
+    splits = pick_splits(tiles0, 148, std::min<i64>(want, j.KB / 16), std::min<i64>(j.KB / 16, 32));
   }
   // Long K: one split per exact int32 segment, slices ordered split-major, so
   // every wave of 148 items streams one K-chunk of its panels (~100 MB at
@@ -631,7 +649,7 @@ int launch_gemm_rns_rows(const Job& j, const void* apack, const void* bpack, dou
   int splits = 1;
   if (tiles0 > 0 && tiles0 < 74) {
     const i64 want = (74 + tiles0 - 1) / tiles0;
-    splits = static_cast<int>(std::max<i64>(1, std::min<i64>({want, j.KB / 16, 32})));
+    splits = pick_splits(tiles0, 74, std::min<i64>(want, j.KB / 16), std::min<i64>(j.KB / 16, 32));
   }
   if (j.KB > q.seg_kb) splits = std::max<int>(splits, (j.KB + q.seg_kb - 1) / q.seg_kb);
   q.kb_per_split = (j.KB + splits - 1) / splits;
