@@ -1009,7 +1009,13 @@ void product_host(const ProductArgs& a, int ngpus, fpmm_b200_timing* tm) {
     const i64 bytes = 8 * (a.m * a.k + a.m * a.n);
     const int want = bytes >= (i64{64} << 20) ? DeviceCtx::kChunks : 1;
     const i64 tiles = (a.m + j.BM - 1) / j.BM;
-    const i64 chunk_rows = ((tiles + want - 1) / want) * j.BM;
+    // ...but each chunk keeps >= 2 waves of output tiles on the SMs (CTA pairs
+    // for RNS): smaller chunks fall back to split-K, whose slices multiply the
+    // RNS residue traffic (measured: 16 chunks of 512 rows ran the 8192^3
+    // compute 2.8x slower than one launch)
+    const i64 slots = j.engine == kRns ? 74 : 148;
+    const i64 min_blocks = std::max<i64>(1, (2 * slots + j.NB - 1) / std::max(j.NB, 1));
+    const i64 chunk_rows = std::max<i64>((tiles + want - 1) / want, min_blocks) * j.BM;
     const int nch = static_cast<int>((a.m + chunk_rows - 1) / chunk_rows);
     int* err = nullptr;
     if (chk) {
