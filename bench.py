@@ -152,7 +152,7 @@ def run_reference(args, bits_list):
         "impl": "reference", "metric": "effective modular GFLOP/s (2mnk/s) over the prime-bitsize sweep",
         "value": round(v, 3), "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(S / args.steps * 1e3, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference random_mat)",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference random_mat)",
         "config": {"workload": args.workload, "m": m, "k": k, "n": n, "bits": [bits_list[0], bits_list[-1]],
                    "sample_dim": CPU_SAMPLE_DIM, "rule": "plan_for_modulus (b=2 scan fix)"},
         "cpu_baseline": {"value": round(v, 3), "unit": "GFLOP/s", "cores": threads, "kind": "reference",
