@@ -172,6 +172,8 @@ def main():
     ap.add_argument("--workload", default="sweep8192", choices=sorted(WORKLOADS))
     ap.add_argument("--bits", default="20-52")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="use the one-process-per-GPU NCCL path even at world size 1 (testing)")
     ap.add_argument("--streams", type=int, default=1,
                     help="streams the sweep's independent products alternate between (N=1); measured: 2-3 "
                          "streams overlap packing/CRT with the tensor kernel but run 3%% slower under the "
@@ -202,7 +204,10 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     part = None
-    if world > 1:
+    # the one-process-per-GPU path (NCCL broadcast of B, gather of C); --force-dist
+    # runs it at world size 1 too (under torchrun --nproc-per-node 1), as a test
+    dist = world > 1 or args.force_dist
+    if dist:
         import torch.distributed as td
         td.init_process_group("nccl", device_id=dev)
         part = D.init_from_torch(local)
@@ -240,7 +245,7 @@ def main():
     # optionally, independent products alternate between streams (each with its
     # own library workspaces) so one product's packing / CRT runs beside
     # another's tensor-core kernel; one stream under torchrun (NCCL ops in order)
-    nstreams = max(1, args.streams) if world == 1 else 1
+    nstreams = max(1, args.streams) if not dist else 1
     streams = [stream] + [torch.cuda.Stream(device=dev) for _ in range(nstreams - 1)]
     Cbufs = [Cbuf] + ([torch.empty_like(Cbuf) for _ in range(nstreams - 1)] if Cbuf is not None else [])
     launches = [0]
@@ -250,7 +255,7 @@ def main():
         fl = eng_flags[engine] | (0 if record is not None else F.ASYNC)
         for idx, (b, p, u, v, lam, _) in enumerate(probs):
             tm = F.Timing()
-            if world == 1:
+            if not dist:
                 sidx = idx % nstreams if record is None else 0
                 F.mw_product_device(A[b], B[b], Cbufs[sidx], p, u, v, lam, stream=streams[sidx], flags=fl,
                                     timing=tm if record is not None else None)
@@ -265,7 +270,7 @@ def main():
                 record[b] = (tm.gemm_ms, tm.engine, tm.words, tm.launches, tm.recon_ms, tm.pack_ms)
 
     def barrier():
-        if world > 1:
+        if dist:
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
@@ -292,7 +297,7 @@ def main():
         e1.record(stream)
         barrier()
     elapsed_ms = e0.elapsed_time(e1)
-    if world > 1:
+    if dist:
         t = torch.tensor([elapsed_ms], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         elapsed_ms = float(t.item())
@@ -369,7 +374,7 @@ def main():
     # end to end through the public host-buffer API (pinned memory), one step
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(F, D, torch, np, probs, A, B, rows, m, k, n, world, rank, part,
+        e2e = run_e2e(F, D, torch, np, probs, A, B, rows, m, k, n, dist, rank, part,
                       eng_flags[args.engine])
 
     cpu = None
@@ -409,12 +414,12 @@ def main():
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist:
         D.finalize()
         torch.distributed.destroy_process_group()
 
 
-def run_e2e(F, D, torch, np, probs, A, B, rows, m, k, n, world, rank, part, flags):
+def run_e2e(F, D, torch, np, probs, A, B, rows, m, k, n, dist, rank, part, flags):
     """E: the sweep through the host-buffer public API.  Each product's timed
     region covers H2D of its inputs from pinned memory, the product and the
     D2H of C.  Inputs are staged into the pinned buffers outside the timer."""
@@ -430,7 +435,7 @@ def run_e2e(F, D, torch, np, probs, A, B, rows, m, k, n, world, rank, part, flag
     # untimed warm-up call: allocates the library's staging buffers
     b, p, u, v, lam, _ = max(probs, key=lambda t: t[2] * t[3])
     r0, rn = rows[b]
-    if world == 1:
+    if not dist:
         F.mw_product(hA.numpy(), hB.numpy(), u, v, lam, F.FpContext.make(p), out=hC.numpy(), flags=flags)
     else:
         D.mw_product_host(hA[:rn], hB, hC, p, u, v, lam, m, root=0, scratch=scratch, flags=flags)
@@ -440,17 +445,17 @@ def run_e2e(F, D, torch, np, probs, A, B, rows, m, k, n, world, rank, part, flag
         if rank == 0:
             hB.copy_(B[b])
         torch.cuda.synchronize()
-        if world > 1:
+        if dist:
             torch.distributed.barrier()
         t0 = time.perf_counter()
-        if world == 1:
+        if not dist:
             F.mw_product(hA.numpy(), hB.numpy(), u, v, lam, F.FpContext.make(p), out=hC.numpy(),
                          flags=flags)
         else:
             D.mw_product_host(hA[:rn], hB, hC, p, u, v, lam, m, root=0, scratch=scratch, flags=flags)
             torch.distributed.barrier()
         dt = time.perf_counter() - t0
-        if world > 1:
+        if dist:
             t = torch.tensor([dt], device="cuda")
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             dt = float(t.item())
@@ -460,7 +465,7 @@ def run_e2e(F, D, torch, np, probs, A, B, rows, m, k, n, world, rank, part, flag
         d2h += 8 * m * n
     return {"value": round(flops / secs / 1e9, 2), "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": round(secs * 1e3, 3),
-            "api": "paper_2601_07508_b200.mw_product (host pinned buffers)" if world == 1
+            "api": "paper_2601_07508_b200.mw_product (host pinned buffers)" if not dist
             else "paper_2601_07508_b200.dist.mw_product_host"}
 
 
