@@ -30,6 +30,26 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# NCCL writes its banner / debug log to stdout; keep stdout to the one JSON
+# line the driver parses
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+
+
+class _StdoutToStderr:
+    """fd-level redirect of stdout to stderr (NCCL prints its version banner
+    with printf at communicator creation)."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+        return False
 
 WORKLOADS = {
     # name: (m, k, n, bits list or None for --bits)
@@ -209,8 +229,9 @@ def main():
     dist = world > 1 or args.force_dist
     if dist:
         import torch.distributed as td
-        td.init_process_group("nccl", device_id=dev)
-        part = D.init_from_torch(local)
+        with _StdoutToStderr():
+            td.init_process_group("nccl", device_id=dev)
+            part = D.init_from_torch(local)
 
     # problems of the step: (bits, p, u, v, lambda)
     probs = []
