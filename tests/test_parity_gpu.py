@@ -311,3 +311,28 @@ def test_dmma_word_choice_at_lambda_collapse(engine, bits, u, v, words):
     tm = F.Timing()
     assert (F.mw_product(A, B, u, v, lam, F.FpContext.make(p), flags=F.DMMA_EXACT_WORDS, timing=tm) == want).all()
     assert tm.words == u * v
+
+
+@pytest.mark.parametrize("bits,u,v", [(34, 1, 2), (40, 2, 2), (52, 2, 2), (52, 2, 3), (42, 1, 4)])
+def test_dmma_reduction_extremes(engine, bits, u, v):
+    """The in-register reduction on inputs that drive the accumulators to
+    their bounds: all-(p-1), alternating (p-1)/0 columns (exact zeros next to
+    maximal sums), residues near p/2 (centred words at both signs) and a zero
+    A, with the engine's own word counts and exactly (u,v)."""
+    if engine != "dmma":
+        pytest.skip("FP64 engine only")
+    p = F.prev_prime(1 << bits)
+    m, k, n = 64, 2000, 72
+    rng = np.random.default_rng(bits * 7 + u)
+    cases = [
+        (np.full((m, k), float(p - 1)), np.full((k, n), float(p - 1))),
+        (np.tile([float(p - 1), 0.0], (m, k // 2)), np.tile([[float(p - 1)], [0.0]], (k // 2, n))),
+        (rng.integers(p // 2 - 3, p // 2 + 4, size=(m, k)).astype(np.float64),
+         rng.integers(p // 2 - 3, p // 2 + 4, size=(k, n)).astype(np.float64)),
+        (np.zeros((m, k)), rng.integers(0, p, size=(k, n)).astype(np.float64)),
+    ]
+    for A, B in cases:
+        want = O.exact_mod_gemm(A, B, p)
+        for fl in (0, F.DMMA_EXACT_WORDS):
+            C = F.mw_product(A, B, u, v, ref_lambda(u, v, p, k), F.FpContext.make(p), flags=fl)
+            assert (C == want).all(), (bits, u, v, fl)
