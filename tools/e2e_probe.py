@@ -38,3 +38,30 @@ for r in range(3):
     F.mw_product(hA.numpy(), hB.numpy(), pl.u, pl.v, pl.lambda_, F.FpContext.make(p), out=hC.numpy(), timing=tm)
     dt = time.perf_counter() - t0
     print("wall %.2f ms" % (dt * 1e3), {k: round(v, 3) if isinstance(v, float) else v for k, v in tm.as_dict().items()})
+
+# sweep mode (as bench.py's e2e leg): per-bitsize wall time with and without
+# refreshing the pinned inputs from the device between calls
+if len(sys.argv) > 3 and sys.argv[3] == "sweep":
+    for refresh in (False, True):
+        tot = 0.0
+        per = []
+        for b in range(20, 53):
+            p = F.prev_prime(1 << b)
+            pl = F.plan_for_modulus(p, n, n, n)
+            if refresh:
+                F.random_residues_device(dA, p, b)
+                hA.copy_(dA)
+                hB.copy_(dA)
+            else:
+                F.random_residues_device(d, p, b)  # keep the inputs valid residues for p
+                hA.copy_(d)
+                hB.copy_(d)
+            torch.cuda.synchronize()
+            tm = F.Timing()
+            t0 = time.perf_counter()
+            F.mw_product(hA.numpy(), hB.numpy(), pl.u, pl.v, pl.lambda_, F.FpContext.make(p), out=hC.numpy(),
+                         timing=tm)
+            dt = time.perf_counter() - t0
+            tot += dt
+            per.append((b, round(dt * 1e3, 2), round(tm.h2d_ms, 2), round(tm.gemm_ms, 2), round(tm.total_ms, 2)))
+        print("refresh" if refresh else "plain", "sweep %.1f ms" % (tot * 1e3), per)
