@@ -347,6 +347,8 @@ def main():
     }
     for eng in ("auto", "i8", "rns", "dmma"):
         rec = {}
+        if eng != args.engine:
+            step(eng)  # untimed: first launches of this engine's kernels (lazy module loading)
         step(eng, record=rec)
         torch.cuda.synchronize()
         per_bits = {}

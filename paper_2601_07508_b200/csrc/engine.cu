@@ -38,7 +38,11 @@ namespace {
 
 std::recursive_mutex g_mu;
 
-// grow-only device buffer
+// grow-only device buffer.  A grow is a cudaFree + cudaMalloc that
+// serialises the device (hundreds of ms for GB-sized workspaces), so it
+// over-allocates by 25%: a bitsize sweep, whose RNS moduli count rises one at
+// a time, then regrows once or twice instead of at every new count.  The
+// exact size is the fallback when the padded one does not fit.
 struct DevBuf {
   void* ptr = nullptr;
   size_t bytes = 0;
@@ -47,11 +51,20 @@ struct DevBuf {
       if (ptr) cudaFree(ptr);
       ptr = nullptr;
       bytes = 0;
-      if (cudaMalloc(&ptr, std::max<size_t>(need, 256)) != cudaSuccess) {
+      need = std::max<size_t>(need, 256);
+      constexpr size_t kRound = size_t{2} << 20;
+      const size_t padded = (need + need / 4 + kRound - 1) / kRound * kRound;
+      if (cudaMalloc(&ptr, padded) == cudaSuccess) {
+        bytes = padded;
+      } else {
         cudaGetLastError();
-        throw Failure(FPMM_B200_ENOMEM, "device allocation of " + std::to_string(need) + " bytes failed");
+        if (cudaMalloc(&ptr, need) != cudaSuccess) {
+          cudaGetLastError();
+          ptr = nullptr;
+          throw Failure(FPMM_B200_ENOMEM, "device allocation of " + std::to_string(need) + " bytes failed");
+        }
+        bytes = need;
       }
-      bytes = std::max<size_t>(need, 256);
     }
     return ptr;
   }
