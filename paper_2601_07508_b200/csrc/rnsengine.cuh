@@ -106,6 +106,12 @@ __device__ __forceinline__ uint32_t mod_small(uint32_t s, uint32_t negm, uint32_
   return __umulhi(s, magic) * negm + s;
 }
 
+// four values < 256 -> one little-endian word, by byte permutes (byte 3 of
+// r0 / r2 is zero and fills the upper bytes of the halves)
+__device__ __forceinline__ uint32_t pack4(uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3) {
+  return __byte_perm(__byte_perm(r0, r1, 0x3340), __byte_perm(r2, r3, 0x3340), 0x5410);
+}
+
 // x < 2^52 as two words of base-256 digits: lo = digits 0..3, hi = digits
 // 4..6 plus the centring flag [x > p/2] in byte 3.  The residue of the
 // centred value mod m is then dp4a(lo, wlo) + dp4a(hi, whi) (< 2^19) mod m.
@@ -124,12 +130,17 @@ __device__ __forceinline__ void digits16(const double (&xs)[16], double half_p, 
 __device__ __forceinline__ uint4 residues16(const uint32_t (&lo)[16], const uint32_t (&hi)[16], const PackParams& P,
                                             int i) {
   const uint32_t nm = P.negm[i], wl = P.wlo[i], wh = P.whi[i], mg = P.magic[i];
-  uint32_t w[4] = {0, 0, 0, 0};
+  uint32_t r[16];
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
     const uint32_t s = __dp4a(lo[e], wl, __dp4a(hi[e], wh, 0u));  // < 2^19
-    w[e / 4] |= mod_small(s, nm, mg) << (8 * (e % 4));
+    r[e] = mod_small(s, nm, mg);
   }
+  // byte packing with PRMT (ALU pipe): dp4a and the IMADs of mod_small
+  // already saturate the FMA-heavy pipe, where shift-by-IMAD would also go
+  uint32_t w[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) w[q] = pack4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
   return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
@@ -249,14 +260,14 @@ __device__ __forceinline__ void park32(const uint32_t (&v)[32], uint32_t m, uint
   uint32_t w[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
-    uint32_t word = 0;
+    uint32_t r[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const uint32_t t = v[q * 4 + e];
       const uint32_t s = (t >> 16) * c16 + (t & 0xFFFFu);  // < 2^24 <= 2^32 / m, == t mod m
-      word |= mod_small(s, negm, magic) << (8 * e);
+      r[e] = mod_small(s, negm, magic);
     }
-    w[q] = word;
+    w[q] = pack4(r[0], r[1], r[2], r[3]);
   }
   if (acc) {  // earlier K segments: add the parked residues mod m
     const uint4 o0 = *dst0, o1 = *dst1;

@@ -23,6 +23,9 @@ KEYS = [
     "smsp__inst_executed.sum", "launch__shared_mem_per_block_dynamic",
     "sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active",
     "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+    "lts__t_sectors_srcunit_tex_lookup_hit.sum", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
 ]
 
 
