@@ -55,8 +55,13 @@ constexpr int kAStage = kBM * kBK;   // 8 KB: this CTA's 128 rows of A
 constexpr int kBStage = kBH * kBK;   // 8 KB: this CTA's 128 columns of B
 constexpr int kStageBytes = kAStage + kBStage;
 constexpr int kStages = 12;
-constexpr int kThreads = 320;        // 10 warps
-constexpr int kEpiWarps = 8;
+#ifndef FPMM_B200_RNS_EPI_WARPS
+#define FPMM_B200_RNS_EPI_WARPS 8
+#endif
+constexpr int kEpiWarps = FPMM_B200_RNS_EPI_WARPS;  // 8 or 16: 4 TMEM lane quadrants x column groups
+constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr int kEpiCols = 4 * kNT / kEpiWarps;        // accumulator columns per epilogue warp
+static_assert(kEpiWarps == 8 || kEpiWarps == 16, "epilogue warps");
 constexpr int kSmem = kStages * kStageBytes + 1024;
 constexpr int kSlotPerMod = kBM * kNT;  // scratch bytes per modulus per CTA tile (32 KB)
 constexpr int kGroup = 16;              // pair-tile rows per rasterisation group
@@ -77,6 +82,8 @@ struct Params {
   int kb_per_split;  // split-K: k-blocks per slice
   int splits;
   int group;         // pair-tile rows per rasterisation group
+  int small_t;       // seg_kb * kBK * 255^2 < 2^24: products reduce without the 16-bit split
+  unsigned epi_sleep_ns;  // epilogue's accumulator wait: sleep between polls (ns), 0 = suspending try_wait
   i64 split_stride;
   unsigned long long p, mu;            // Barrett: mu = floor(2^64 / p)
   unsigned long long two32, two32_sh;  // 2^32 mod p and its Shoup quotient
@@ -255,6 +262,9 @@ __device__ __forceinline__ uint4* scratch_at(uint8_t* slot, int i, int half, int
 }
 
 // Reduce 32 TMEM columns (one tcgen05.ld) mod m and park them as 2 x 16 bytes.
+// SMALL: every product is below 2^24 (K segments of <= 258 terms, e.g. the
+// k = 256 outer-product shape), so mod_small applies to it directly.
+template <bool SMALL>
 __device__ __forceinline__ void park32(const uint32_t (&v)[32], uint32_t m, uint32_t negm, uint32_t c16, uint32_t magic,
                                        bool acc, uint4* dst0, uint4* dst1) {
   uint32_t w[8];
@@ -264,7 +274,7 @@ __device__ __forceinline__ void park32(const uint32_t (&v)[32], uint32_t m, uint
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const uint32_t t = v[q * 4 + e];
-      const uint32_t s = (t >> 16) * c16 + (t & 0xFFFFu);  // < 2^24 <= 2^32 / m, == t mod m
+      const uint32_t s = SMALL ? t : (t >> 16) * c16 + (t & 0xFFFFu);  // < 2^24 <= 2^32 / m, == t mod m
       r[e] = mod_small(s, negm, magic);
     }
     w[q] = pack4(r[0], r[1], r[2], r[3]);
@@ -461,8 +471,14 @@ __device__ __forceinline__ uint32_t peer_addr(const void* p, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(out) : "r"(dev::smem_u32(p)), "r"(rank));
   return out;
 }
+// Arrive on a (possibly remote) barrier of the pair, default .release.cta
+// semantics.  Only the epilogue's TMEM drain uses it: its tcgen05.ld values are
+// already in registers (tcgen05.wait::ld + fence::before_thread_sync), so the
+// MMA may overwrite the accumulator.  A .release.cluster arrive also waited for
+// the thread's earlier streaming stores of parked residues to reach L2 (an
+// ERRBAR: 24% of the stall samples at k = 256, where passes are short).
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   asm volatile(
@@ -619,7 +635,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
     // residue bytes per element back and runs the CRT into C.  Each thread
     // only ever reads bytes it wrote itself.
     const int quad = warp % 4;
-    const int half = (warp - 2) / 4;
+    const int col0 = ((warp - 2) / 4) * kEpiCols;  // this warp's first accumulator column
+    const int half = col0 / (kNT / 2);
     const int row_in_tile = quad * 32 + lane;
     const uint32_t tlane = static_cast<uint32_t>(quad * 32) << 16;
     const uint32_t leader_tmem_empty = peer_addr(tmem_empty, 0);
@@ -634,21 +651,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
         uint8_t* slot = P.scratch + (static_cast<i64>(t) * 2 + rank) * P.nmod * kSlotPerMod;
         for (int seg = 0; seg < nseg; ++seg, ++pass) {
           const int b = pass & 1;
-          dev::mbar_wait_sleep(&tmem_full[b], (pass >> 1) & 1, 256);
+          if (P.epi_sleep_ns) dev::mbar_wait_sleep(&tmem_full[b], (pass >> 1) & 1, P.epi_sleep_ns);
+          else dev::mbar_wait(&tmem_full[b], (pass >> 1) & 1);
           i8::fence_after();
           const uint32_t tcol = tbase + tlane + b * kNT + half * (kNT / 2);
 #pragma unroll 1
-          for (int c0 = 0; c0 < kNT / 2; c0 += 32) {
+          for (int c0 = col0 % (kNT / 2); c0 < col0 % (kNT / 2) + kEpiCols; c0 += 32) {
             uint32_t v[32];
             i8::tmem_ld32(tcol + c0, v);
             i8::tmem_wait_ld();
-            if (c0 + 32 == kNT / 2) {  // every column of this buffer is in registers: release it
+            if (c0 + 32 == col0 % (kNT / 2) + kEpiCols) {  // all of this warp's columns are in registers: release
               i8::fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive_cluster(leader_tmem_empty + b * 8);
             }
-            park32(v, m, nm, c16, mg, seg > 0, scratch_at(slot, i, half, c0 / 16, row_in_tile),
-                     scratch_at(slot, i, half, c0 / 16 + 1, row_in_tile));
+            uint4* d0 = scratch_at(slot, i, half, c0 / 16, row_in_tile);
+            uint4* d1 = scratch_at(slot, i, half, c0 / 16 + 1, row_in_tile);
+            if (P.small_t) park32<true>(v, m, nm, c16, mg, seg > 0, d0, d1);
+            else park32<false>(v, m, nm, c16, mg, seg > 0, d0, d1);
           }
         }
       }

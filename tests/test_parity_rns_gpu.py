@@ -169,3 +169,22 @@ def test_rns_row_blocks_under_a_residue_budget(monkeypatch):
     C = F.mw_product(A, B, 2, 2, 7, F.FpContext.make(p), flags=RNS, timing=tm)
     assert (C == O.exact_mod_gemm(A, B, p)).all()
     assert tm.launches > 4  # several GEMM + CRT pairs
+
+
+@pytest.mark.parametrize("bits", [8, 20, 40, 52])
+@pytest.mark.parametrize("k", [64, 256])
+def test_rns_short_k_extremes(bits, k):
+    """K segments of <= 258 terms (the k = 256 outer-product shape): the
+    epilogue reduces each product below 2^24 without the 16-bit split.  Both
+    signs of the extreme X = +-K floor(p/2)^2, plus random residues."""
+    p = F.prev_prime(1 << bits)
+    h = p // 2
+    m, n = 300, 260
+    rng = np.random.default_rng(bits + k)
+    cases = [(np.full((m, k), float(h)), np.full((k, n), float(h))),
+             (np.full((m, k), float(h)), np.full((k, n), float(h + 1))),
+             (rng.integers(0, p, size=(m, k)).astype(np.float64), rng.integers(0, p, size=(k, n)).astype(np.float64))]
+    pl = F.plan_for_modulus(p, m, k, n)
+    for A, B in cases:
+        C = F.mw_product(A, B, pl.u, pl.v, min(pl.lambda_, k), F.FpContext.make(p), flags=RNS)
+        assert (C == O.exact_mod_gemm(A, B, p)).all(), (bits, k)
