@@ -222,6 +222,14 @@ int fpmm_b200_dist_finalize(void);
 /* Row partition used by the partitioner: rows [*row0, *row0 + *rows) of m. */
 int fpmm_b200_dist_rows(int64_t m, int nranks, int rank, int u, int v, int64_t* row0,
                         int64_t* rows);
+/* Row chunks [starts[i], starts[i] + lens[i]) of a rank block of `rows` rows
+ * in which the row-sharded product computes and, with a gather, ships C to
+ * root (chunk i's transfer overlaps chunk i+1's compute).  At most
+ * FPMM_B200_DIST_MAX_CHUNKS chunks; the same function on every rank, so root
+ * knows each rank's chunks. */
+#define FPMM_B200_DIST_MAX_CHUNKS 4
+int fpmm_b200_dist_chunks(int64_t m, int64_t k, int64_t n, uint64_t p, int u, int v, unsigned flags,
+                          int64_t rows, int* count, int64_t* starts, int64_t* lens);
 /* Row-sharded product.  Every rank passes its own A row block (dA_rows:
  * rows x k, this rank's slice from fpmm_b200_dist_rows) and receives its C
  * row block in dC_rows.  dB (k x n) is read on `root` only and its words are

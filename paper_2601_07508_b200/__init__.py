@@ -162,6 +162,8 @@ def lib():
         "fpmm_b200_dist_init": (i32, [vp, i32, i32, i32]),
         "fpmm_b200_dist_finalize": (i32, []),
         "fpmm_b200_dist_rows": (i32, [i64, i32, i32, i32, i32, _i64p, _i64p]),
+        "fpmm_b200_dist_chunks": (i32, [i64, i64, i64, u64, i32, i32, C.c_uint, i64, C.POINTER(C.c_int),
+                                        _i64p, _i64p]),
         "fpmm_b200_dist_mw_product_device": (i32, [vp, i64, vp, i64, vp, i64, vp, i64, i64, i64, i64,
                                                    u64, i32, i32, u64, i32, vp, C.c_uint,
                                                    C.POINTER(Timing)]),

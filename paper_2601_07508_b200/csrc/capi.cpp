@@ -261,6 +261,13 @@ int fpmm_b200_dist_rows(int64_t m, int nranks, int rank, int u, int v, int64_t* 
     *rows = b;
   });
 }
+int fpmm_b200_dist_chunks(int64_t m, int64_t k, int64_t n, uint64_t p, int u, int v, unsigned flags,
+                          int64_t rows, int* count, int64_t* starts, int64_t* lens) {
+  return guarded([&] {
+    if (rows < 0) throw Failure(FPMM_B200_EERROR, "rows must be nonnegative");
+    dist_chunks(m, k, n, p, u, v, flags, rows, count, starts, lens);
+  });
+}
 int fpmm_b200_dist_mw_product_device(const double* dA_rows, int64_t lda, const double* dB,
                                      int64_t ldb, double* dC_rows, int64_t ldc, double* dC_full,
                                      int64_t ldc_full, int64_t m, int64_t k, int64_t n, uint64_t p,

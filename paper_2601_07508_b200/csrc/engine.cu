@@ -1429,6 +1429,36 @@ void dist_rows(i64 m, int nranks, int rank, int u, int v, i64* row0, i64* rows) 
   *rows = std::min<i64>(m, r0 + per) - r0;
 }
 
+// Row chunks of one rank's block for the overlapped gather: chunk c's C rows
+// go to root (NCCL send/recv on a second stream) while chunk c+1 computes.
+// Whole row tiles, each chunk >= 2 waves of the engine's output tiles (CTA
+// pairs for RNS; smaller launches fall back to split-K), at most 4 chunks.
+// A pure function of (job, rows): root derives every rank's chunks itself.
+constexpr int kGatherChunks = FPMM_B200_DIST_MAX_CHUNKS;
+std::vector<std::pair<i64, i64>> gather_chunks(const Job& j, i64 rows) {
+  std::vector<std::pair<i64, i64>> out;
+  if (rows <= 0) return out;
+  const i64 slots = j.engine == kRns ? 74 : 148;
+  const i64 min_tiles = std::max<i64>(1, (2 * slots + j.NB - 1) / std::max(j.NB, 1));
+  const i64 tiles = (rows + j.BM - 1) / j.BM;
+  i64 cap = kGatherChunks;
+  if (const char* e = std::getenv("FPMM_B200_DIST_CHUNKS")) cap = std::max(1, std::min(kGatherChunks, std::atoi(e)));
+  const i64 nch = std::max<i64>(1, std::min<i64>(cap, tiles / min_tiles));
+  const i64 per = (tiles + nch - 1) / nch * j.BM;
+  for (i64 r = 0; r < rows; r += per) out.emplace_back(r, std::min<i64>(per, rows - r));
+  return out;
+}
+
+void dist_chunks(i64 m, i64 k, i64 n, u64 p, int u, int v, unsigned flags, i64 rows, int* count, i64* starts,
+                 i64* lens) {
+  context_check(p, (flags & FPMM_B200_ALLOW_COMPOSITE) != 0);
+  const Job j = make_job(std::max<i64>(m, 1), std::max<i64>(k, 1), std::max<i64>(n, 1), p, u, v, resolve_engine(flags),
+                         (flags & FPMM_B200_DMMA_EXACT_WORDS) != 0);
+  const auto ch = gather_chunks(j, rows);
+  *count = static_cast<int>(ch.size());
+  for (size_t i = 0; i < ch.size(); ++i) starts[i] = ch[i].first, lens[i] = ch[i].second;
+}
+
 void dist_product_device(const double* dA_rows, i64 lda, const double* dB, i64 ldb, double* dC_rows,
                          i64 ldc, double* dC_full, i64 ldc_full, i64 m, i64 k, i64 n, u64 p, int u,
                          int v, u64 lambda, int root, void* stream, unsigned flags,
@@ -1475,31 +1505,62 @@ void dist_product_device(const double* dA_rows, i64 lda, const double* dB, i64 l
     NCCL_OK(nccl().Broadcast(bpack, bpack, j.bpack_bytes, ncclUint8, root, g_dist.comm, s));
   }
   CUDA_OK(cudaEventRecord(c.ev[2], s));
-  const int gl = rn > 0 ? launch_gemm(j, apack, bpack, dC_rows, ldc, rn, s, ws) : 0;
+  // the product in row chunks; with a gather, chunk c's rows travel to root
+  // on stream s_out (NCCL P2P) while chunk c+1 computes on s.  Every NCCL call
+  // of this product is issued in the same order on every rank: the broadcast
+  // (stream s, complete before any chunk's compute), then one group per chunk
+  // index on s_out.
+  const auto mine = dC_full ? gather_chunks(j, rn) : std::vector<std::pair<i64, i64>>{{0, rn}};
+  int gl = 0;
+  for (size_t ci = 0; ci < mine.size(); ++ci) {
+    const i64 o = mine[ci].first, l = mine[ci].second;
+    if (l <= 0) continue;
+    gl += launch_gemm(j, static_cast<uint8_t*>(apack) + static_cast<size_t>(o / j.BM) * j.per_rb_bytes, bpack,
+                      dC_rows + o * ldc, ldc, l, s, ws);
+    if (dC_full) CUDA_OK(cudaEventRecord(c.ev_out[ci], s));
+  }
   CUDA_OK(cudaEventRecord(c.ev[3], s));
   int launches = (rn > 0 ? 1 + gl : 0) + (g_dist.rank == root || raw ? 1 : 0);
   if (dC_full) {
     // gather row blocks to root (grouped point-to-point; NCCL has no gather)
     if (ldc != n || (g_dist.rank == root && ldc_full != n))
       throw Failure(FPMM_B200_EERROR, "dist_mw_product: gather needs dense row blocks (ld == n)");
-    NCCL_OK(nccl().GroupStart());
-    if (g_dist.rank == root) {
+    cudaStream_t so = c.s_out;
+    CUDA_OK(cudaStreamWaitEvent(so, c.ev[2], 0));  // root's copies / recvs follow this call's earlier work
+    std::vector<std::vector<std::pair<i64, i64>>> theirs(g_dist.nranks);
+    std::vector<i64> q0s(g_dist.nranks, 0);
+    size_t rounds = mine.size();
+    if (g_dist.rank == root)
       for (int r = 0; r < g_dist.nranks; ++r) {
-        i64 q0 = 0, qn = 0;
-        dist_rows(m, g_dist.nranks, r, u, v, &q0, &qn);
-        if (qn == 0) continue;
-        if (r == root) {
-          if (dC_full + q0 * ldc_full != dC_rows)
-            CUDA_OK(cudaMemcpyAsync(dC_full + q0 * ldc_full, dC_rows, sizeof(double) * qn * n,
-                                    cudaMemcpyDeviceToDevice, s));
-        } else {
-          NCCL_OK(nccl().Recv(dC_full + q0 * ldc_full, static_cast<size_t>(qn * n), ncclDouble, r, g_dist.comm, s));
-        }
+        i64 qn = 0;
+        dist_rows(m, g_dist.nranks, r, u, v, &q0s[r], &qn);
+        theirs[r] = gather_chunks(j, qn);
+        rounds = std::max(rounds, theirs[r].size());
       }
-    } else if (rn > 0) {
-      NCCL_OK(nccl().Send(dC_rows, static_cast<size_t>(rn * n), ncclDouble, root, g_dist.comm, s));
+    for (size_t ci = 0; ci < rounds; ++ci) {
+      if (ci < mine.size()) CUDA_OK(cudaStreamWaitEvent(so, c.ev_out[ci], 0));
+      NCCL_OK(nccl().GroupStart());
+      if (g_dist.rank == root) {
+        for (int r = 0; r < g_dist.nranks; ++r) {
+          if (ci >= theirs[r].size()) continue;
+          const i64 row = q0s[r] + theirs[r][ci].first, len = theirs[r][ci].second;
+          if (r == root) {
+            if (dC_full + q0s[r] * ldc_full != dC_rows)
+              CUDA_OK(cudaMemcpyAsync(dC_full + row * ldc_full, dC_rows + theirs[r][ci].first * ldc,
+                                      sizeof(double) * len * n, cudaMemcpyDeviceToDevice, so));
+          } else {
+            NCCL_OK(nccl().Recv(dC_full + row * ldc_full, static_cast<size_t>(len * n), ncclDouble, r, g_dist.comm,
+                                so));
+          }
+        }
+      } else if (ci < mine.size()) {
+        NCCL_OK(nccl().Send(dC_rows + mine[ci].first * ldc, static_cast<size_t>(mine[ci].second * n), ncclDouble, root,
+                            g_dist.comm, so));
+      }
+      NCCL_OK(nccl().GroupEnd());
     }
-    NCCL_OK(nccl().GroupEnd());
+    CUDA_OK(cudaEventRecord(c.ev[5], so));
+    CUDA_OK(cudaStreamWaitEvent(s, c.ev[5], 0));  // the call completes on its own stream
   }
   CUDA_OK(cudaEventRecord(c.ev[4], s));
   if (err) check_err_flag(c, s);

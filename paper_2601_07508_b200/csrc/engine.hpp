@@ -70,6 +70,8 @@ void nccl_unique_id(void* id);
 void dist_init(const void* id, int nranks, int rank, int device);
 void dist_finalize();
 void dist_rows(i64 m, int nranks, int rank, int u, int v, i64* row0, i64* rows);
+void dist_chunks(i64 m, i64 k, i64 n, u64 p, int u, int v, unsigned flags, i64 rows, int* count, i64* starts,
+                 i64* lens);
 void dist_product_device(const double* dA_rows, i64 lda, const double* dB, i64 ldb, double* dC_rows,
                          i64 ldc, double* dC_full, i64 ldc_full, i64 m, i64 k, i64 n, u64 p, int u,
                          int v, u64 lambda, int root, void* stream, unsigned flags,

@@ -33,6 +33,16 @@ class Partitioner:
         _check(lib().fpmm_b200_dist_rows(m, self.nranks, r, u, v, C.byref(a), C.byref(b)))
         return a.value, b.value
 
+    @staticmethod
+    def chunks_for(rows: int, m: int, k: int, n: int, p: int, u: int, v: int, flags: int = 0):
+        """[(start, len)] row chunks of a `rows`-row block: the order in which
+        the gathered product computes and ships C to root (fpmm_b200_dist_chunks)."""
+        cnt = C.c_int()
+        st = (C.c_int64 * 4)()
+        ln = (C.c_int64 * 4)()
+        _check(lib().fpmm_b200_dist_chunks(m, k, n, p, u, v, flags, rows, C.byref(cnt), st, ln))
+        return [(st[i], ln[i]) for i in range(cnt.value)]
+
 
 _inited = False
 

@@ -63,3 +63,39 @@ def test_in_process_ngpus1_equals_default():
     assert (C == O.exact_mod_gemm(A, B, p)).all()
     with pytest.raises(F.Error):
         F.mw_product(A, B, pl.u, pl.v, pl.lambda_, F.FpContext.make(p), ngpus=F.device_count() + 1)
+
+
+@pytest.mark.parametrize("engine,shape,bits", [("rns", (8192, 64, 8192), 52), ("dmma", (80000, 8, 40), 20),
+                                               ("i8", (8192, 64, 2048), 44)])
+def test_dist_world1_chunked_gather(engine, shape, bits):
+    """A rank block large enough for several row chunks: the product runs chunk
+    by chunk and each chunk's C rows are shipped to root on the second stream
+    (at world size 1, root's own copies).  C on root equals the
+    single-process product bitwise and passes Freivalds."""
+    import torch
+    import torch.distributed as td
+    from paper_2601_07508_b200 import dist as D
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()))
+    td.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        D.init_from_torch(0)
+        m, k, n = shape
+        p = F.prev_prime(1 << bits)
+        pl = F.plan_for_modulus(p, m, k, n)
+        eng = {"i8": F.ENGINE_I8, "rns": F.ENGINE_RNS, "dmma": F.ENGINE_DMMA}[engine]
+        assert len(D.Partitioner.chunks_for(m, m, k, n, p, pl.u, pl.v, eng)) >= 2
+        dA = torch.empty((m, k), dtype=torch.float64, device="cuda")
+        dB = torch.empty((k, n), dtype=torch.float64, device="cuda")
+        F.random_residues_device(dA, p, 11)
+        F.random_residues_device(dB, p, 12)
+        dCr = torch.empty((m, n), dtype=torch.float64, device="cuda")
+        dCf = torch.full((m, n), -1.0, dtype=torch.float64, device="cuda")
+        D.mw_product_device(dA, dB, dCr, p, pl.u, pl.v, pl.lambda_, m, root=0, C_full=dCf, flags=eng)
+        ref = torch.empty_like(dCr)
+        F.mw_product_device(dA, dB, ref, p, pl.u, pl.v, pl.lambda_, flags=eng)
+        torch.cuda.synchronize()
+        assert torch.equal(dCr, ref) and torch.equal(dCf, ref)
+        assert O.freivalds(dA.cpu().numpy(), dB.cpu().numpy(), dCf.cpu().numpy(), p, trials=2) == 0
+        D.finalize()
+    finally:
+        td.destroy_process_group()
