@@ -529,16 +529,21 @@ void launch_pack_a(const Job& j, const double* A, i64 lda, i64 rows, void* apack
   CUDA_OK(cudaGetLastError());
 }
 
+// RNS: B's k-blocks [kb0, kb0 + nkb) only (the multi-GPU path's k-chunks); B
+// is the whole k x n matrix, and the residue check covers the chunk's rows.
+void launch_pack_b_rns(const Job& j, const double* B, i64 ldb, void* bpack, int* err, cudaStream_t s, int kb0,
+                       int nkb) {
+  const i64 r0 = static_cast<i64>(kb0) * rns::kBK, r1 = std::min<i64>(j.k, static_cast<i64>(kb0 + nkb) * rns::kBK);
+  if (err && r1 > r0 && j.n > 0)
+    check_residues_kernel<<<grid_for((r1 - r0) * j.n, 256), 256, 0, s>>>(B + r0 * ldb, ldb, r1 - r0, j.n, j.p, err);
+  const i64 tiles = static_cast<i64>(nkb) * (2 * j.NB) * (rns::kBH / 32);
+  rns::pack_b_rns<<<static_cast<unsigned>(std::min<i64>(std::max<i64>(tiles, 1), 148 * 32)), 128, 0, s>>>(
+      B, ldb, j.k, j.n, j.KB, 2 * j.NB, kb0, nkb, j.rpp, static_cast<uint8_t*>(bpack));
+  CUDA_OK(cudaGetLastError());
+}
+
 void launch_pack_b(const Job& j, const double* B, i64 ldb, void* bpack, int* err, cudaStream_t s) {
-  if (j.engine == kRns) {
-    if (err && j.k > 0 && j.n > 0)
-      check_residues_kernel<<<grid_for(j.k * j.n, 256), 256, 0, s>>>(B, ldb, j.k, j.n, j.p, err);
-    const i64 tiles = static_cast<i64>(j.KB) * (2 * j.NB) * (rns::kBH / 32);
-    rns::pack_b_rns<<<static_cast<unsigned>(std::min<i64>(std::max<i64>(tiles, 1), 148 * 32)), 128, 0, s>>>(
-        B, ldb, j.k, j.n, j.KB, 2 * j.NB, j.rpp, static_cast<uint8_t*>(bpack));
-    CUDA_OK(cudaGetLastError());
-    return;
-  }
+  if (j.engine == kRns) return launch_pack_b_rns(j, B, ldb, bpack, err, s, 0, j.KB);
   if (j.engine == kI8) {
     if (err && j.k > 0 && j.n > 0)
       check_residues_kernel<<<grid_for(j.k * j.n, 256), 256, 0, s>>>(B, ldb, j.k, j.n, j.p, err);
@@ -1490,7 +1495,32 @@ void dist_product_device(const double* dA_rows, i64 lda, const double* dB, i64 l
   // element) packed by every rank when that is fewer bytes (the RNS engine
   // above 8 moduli, the FP64 engine at v >= 2) or when BCAST_RAW_B asks
   const bool raw = (flags & FPMM_B200_BCAST_RAW_B) || j.bpack_bytes > static_cast<size_t>(8) * k * n;
-  if (raw) {
+  // RNS with a large raw B: the broadcast runs in k-chunks on stream s_out and
+  // each chunk's residues are packed on s as soon as it lands, so the per-rank
+  // pack of B (about 9 ms at 32768^2) hides under the broadcast.
+  const int bchunks = (raw && j.engine == kRns && static_cast<size_t>(8) * k * n >= (size_t{256} << 20))
+                          ? std::min(4, j.KB) : 1;
+  if (raw && bchunks > 1) {
+    cudaStream_t so = c.s_out;
+    double* dBd = static_cast<double*>(c.b.get(sizeof(double) * k * n));
+    if (g_dist.rank == root)
+      CUDA_OK(cudaMemcpy2DAsync(dBd, n * 8, dB, ldb * 8, n * 8, k, cudaMemcpyDeviceToDevice, s));
+    CUDA_OK(cudaEventRecord(c.ev[6], s));  // B staged; the last call's reads of dBd are done
+    CUDA_OK(cudaStreamWaitEvent(so, c.ev[6], 0));
+    if (rn > 0) launch_pack_a(j, dA_rows, lda, rn, apack, err, s);
+    CUDA_OK(cudaEventRecord(c.ev[1], s));
+    const int per = (j.KB + bchunks - 1) / bchunks;
+    for (int bc = 0; bc < bchunks; ++bc) {
+      const int kb0 = bc * per, nkb = std::min(j.KB, kb0 + per) - kb0;
+      if (nkb <= 0) break;
+      const i64 k0 = static_cast<i64>(kb0) * rns::kBK, k1 = std::min<i64>(k, static_cast<i64>(kb0 + nkb) * rns::kBK);
+      NCCL_OK(nccl().Broadcast(dBd + k0 * n, dBd + k0 * n, static_cast<size_t>((k1 - k0) * n), ncclDouble, root,
+                               g_dist.comm, so));
+      CUDA_OK(cudaEventRecord(c.ev_in[bc], so));
+      CUDA_OK(cudaStreamWaitEvent(s, c.ev_in[bc], 0));
+      launch_pack_b_rns(j, dBd, n, bpack, g_dist.rank == root ? err : nullptr, s, kb0, nkb);
+    }
+  } else if (raw) {
     double* dBd = static_cast<double*>(c.b.get(sizeof(double) * k * n));
     if (g_dist.rank == root)
       CUDA_OK(cudaMemcpy2DAsync(dBd, n * 8, dB, ldb * 8, n * 8, k, cudaMemcpyDeviceToDevice, s));
@@ -1520,7 +1550,7 @@ void dist_product_device(const double* dA_rows, i64 lda, const double* dB, i64 l
     if (dC_full) CUDA_OK(cudaEventRecord(c.ev_out[ci], s));
   }
   CUDA_OK(cudaEventRecord(c.ev[3], s));
-  int launches = (rn > 0 ? 1 + gl : 0) + (g_dist.rank == root || raw ? 1 : 0);
+  int launches = (rn > 0 ? 1 + gl : 0) + (g_dist.rank == root || raw ? bchunks : 0);
   if (dC_full) {
     // gather row blocks to root (grouped point-to-point; NCCL has no gather)
     if (ldc != n || (g_dist.rank == root && ldc_full != n))

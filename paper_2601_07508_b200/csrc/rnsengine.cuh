@@ -201,15 +201,17 @@ __global__ void __launch_bounds__(256) pack_a_rns(const double* __restrict__ A, 
 // B: k x n residues -> N residue planes of 128-column blocks, K-major.
 // Chunk (cb, i, kb), kBStage bytes: [k16 c (4)][column group (16)][column (8)][16 B].
 // A 128-thread block transposes a 64 (k) x 32 (column) tile through shared memory.
+// k-blocks [kb_begin, kb_begin + kb_count) only (the multi-GPU path packs B's
+// k-chunks as their broadcast lands); KB is the layout's k-block count.
 __global__ void __launch_bounds__(128) pack_b_rns(const double* __restrict__ B, i64 ldb, i64 k, i64 n, int KB,
-                                                  int NB128, const __grid_constant__ PackParams P,
-                                                  uint8_t* __restrict__ out) {
+                                                  int NB128, int kb_begin, int kb_count,
+                                                  const __grid_constant__ PackParams P, uint8_t* __restrict__ out) {
   constexpr int SW = 32, SUB = kBH / SW;
   __shared__ double tile[kBK][SW + 1];
-  const i64 tiles = static_cast<i64>(KB) * NB128 * SUB;
+  const i64 tiles = static_cast<i64>(kb_count) * NB128 * SUB;
   for (i64 t = blockIdx.x; t < tiles; t += gridDim.x) {
     const int sb = static_cast<int>(t % SUB);
-    const i64 cb = (t / SUB) % NB128, kb = t / (SUB * static_cast<i64>(NB128));
+    const i64 cb = (t / SUB) % NB128, kb = kb_begin + t / (SUB * static_cast<i64>(NB128));
     __syncthreads();
     for (int e = threadIdx.x; e < kBK * SW; e += blockDim.x) {
       const int kr = e / SW, cc = e % SW;

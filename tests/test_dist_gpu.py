@@ -66,12 +66,14 @@ def test_in_process_ngpus1_equals_default():
 
 
 @pytest.mark.parametrize("engine,shape,bits", [("rns", (8192, 64, 8192), 52), ("dmma", (80000, 8, 40), 20),
-                                               ("i8", (8192, 64, 2048), 44)])
+                                               ("i8", (8192, 64, 2048), 44), ("rns", (8192, 4100, 8192), 52)])
 def test_dist_world1_chunked_gather(engine, shape, bits):
     """A rank block large enough for several row chunks: the product runs chunk
     by chunk and each chunk's C rows are shipped to root on the second stream
-    (at world size 1, root's own copies).  C on root equals the
-    single-process product bitwise and passes Freivalds."""
+    (at world size 1, root's own copies).  The last case also broadcasts its
+    raw B (>= 256 MB, RNS) in k-chunks packed as they land, with a ragged last
+    k-chunk.  C on root equals the single-process product bitwise and passes
+    Freivalds."""
     import torch
     import torch.distributed as td
     from paper_2601_07508_b200 import dist as D
