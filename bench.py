@@ -75,7 +75,10 @@ def parse_bits(s: str):
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clock, power and clock-event (throttle) reasons sampled during the
+    timed region: NVML every 20 ms (nvidia-ml-py), else nvidia-smi every 0.2 s.
+    Samples are [sm_mhz, max_mhz, power_w, hw_slowdown, hw_thermal, sw_thermal,
+    sw_power_cap]."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -84,17 +87,45 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.samples = []
+        self.source = "nvidia-smi"
         self._stop = threading.Event()
         self._t = None
 
+    def _run_nvml(self, nv):
+        h = nv.nvmlDeviceGetHandleByIndex(self.index)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
+        while not self._stop.is_set():
+            try:
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append([float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)), float(mx),
+                                     nv.nvmlDeviceGetPowerUsage(h) / 1000.0] +
+                                    [bool(r & b) for b in bits])
+            except Exception:
+                pass
+            self._stop.wait(0.02)
+
     def _run(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.source = "nvml"
+            try:
+                return self._run_nvml(nv)
+            finally:
+                nv.nvmlShutdown()
+        except Exception:
+            self.source = "nvidia-smi"
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True,
                                      timeout=5).stdout.strip()
                 if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                    f = [x.strip() for x in out.split(",")]
+                    num = lambda x: float(x) if x.replace(".", "").isdigit() else None  # noqa: E731
+                    self.samples.append([num(f[0]), num(f[1]), num(f[2])] + [x.lower() == "active" for x in f[3:7]])
             except Exception:
                 pass
             self._stop.wait(0.2)
@@ -110,15 +141,14 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
-        mx = max(float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit())
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
+        sm = sorted(s[0] for s in self.samples if s[0] is not None)
+        mx = max((s[1] for s in self.samples if s[1] is not None), default=None)
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
-        pw = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and s[3 + i]})
+        pw = [s[2] for s in self.samples if s[2] is not None]
         return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
-                "samples": len(self.samples), "power_w_max": max(pw) if pw else None}
+                "samples": len(self.samples), "source": self.source, "power_w_max": max(pw) if pw else None}
 
 
 # --------------------------------------------------------------- reference
