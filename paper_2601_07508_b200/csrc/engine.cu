@@ -388,6 +388,13 @@ Job make_rns_job(i64 m, i64 k, i64 n, u64 p) {
   cp.two32_sh = q.two32_sh;
   cp.Mp = pl.Mp;
   cp.Mp_sh = q.Mp_sh;
+  {
+    int bits = 0;
+    while (bits < 64 && (u64{1} << bits) < p) ++bits;  // ceil(log2 p)
+    cp.s_shift = std::max(0, bits - 20);
+    cp.inv32 = static_cast<uint32_t>((static_cast<u128>(1) << (cp.s_shift + 32)) / p);
+    cp.Mp_sh32 = static_cast<uint32_t>((static_cast<u128>(pl.Mp) << 32) / p);
+  }
   for (int i = 0; i < j.nmod; ++i) {
     cp.mod[i] = pl.mod[i];
     const u64 g = ((static_cast<u64>(pl.y[i]) << 19) + pl.mod[i] / 2) / pl.mod[i];  // < 2^19

@@ -252,6 +252,13 @@ __device__ __forceinline__ Item item_of(int t, const Params& P) {
   return it;
 }
 
+// a * b + c with a 32 x 32 -> 64-bit product (one IMAD.WIDE.U32)
+__device__ __forceinline__ unsigned long long mad_wide(uint32_t a, uint32_t b, unsigned long long c) {
+  unsigned long long d;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
+  return d;
+}
+
 __device__ __forceinline__ uint64_t barrett(uint64_t x, uint64_t p, uint64_t mu) {
   const uint64_t q = __umul64hi(x, mu);
   uint64_t r = x - q * p;
@@ -320,6 +327,11 @@ struct CrtParams {
   i64 ldc, m, n;
   int MB, NB, nmod, splits, group;
   unsigned long long p, mu, two32, two32_sh, Mp, Mp_sh;
+  // n <= 16 finalisation (S < 16 * 255 * p): q = umulhi(S >> s_shift, inv32)
+  // is floor(S/p) - {0,1,2}; t (M mod p) by a 32-bit Shoup product
+  int s_shift;     // max(0, bits(p) - 20): S >> s_shift < 2^32 and 2^s_shift < p
+  uint32_t inv32;  // floor(2^(s_shift + 32) / p)
+  uint32_t Mp_sh32;  // floor((M mod p) 2^32 / p)
   uint32_t mod[kMaxMod];
   uint32_t wb[kCrtGroups][kCrtPlanes];  // byte b of W_i (b < 7) / g_i (b >= 7) for the group's 4 moduli
 };
@@ -392,11 +404,23 @@ __device__ __forceinline__ void crt_step(const CrtParams& P, int c, i64 colh, do
     const uint32_t tt = (a[8] + (a[9] << 8) + (a[7] >> 8) + 1024u) >> 11;
     // S = sum_i r_i W_i = sum_b 2^(8b) a_b (b < WPL)
     unsigned long long sm;
-    if (P.nmod <= 16) {  // S < 16 * 255 * 2^52 < 2^64: one u64 and one Barrett
-      unsigned long long S = 0;
+    if (P.nmod <= 16) {  // S = sum_i r_i W_i <= 16 * 255 * (p - 1) < 2^64
+      // planes 0..3 by 32x32 -> 64-bit multiply-adds, planes 4..6 on the high
+      // word in 32-bit wrap-around (S < 2^64 makes the sum exact mod 2^64)
+      unsigned long long S = a[0];
 #pragma unroll
-      for (int b = 0; b < WPL; ++b) S += static_cast<unsigned long long>(a[b]) << (8 * b);
-      sm = barrett(S, p, P.mu);
+      for (int b = 1; b < (WPL < 4 ? WPL : 4); ++b) S = mad_wide(a[b], 1u << (8 * b), S);
+      if (WPL > 4) {
+        uint32_t hi = a[4];
+#pragma unroll
+        for (int b = 5; b < WPL; ++b) hi += a[b] << (8 * (b - 4));
+        S += static_cast<unsigned long long>(hi) << 32;
+      }
+      // q = floor(S/p) - {0,1,2}: (S >> s) < 2^32, inv32 = floor(2^(s+32)/p)
+      const uint32_t q = __umulhi(static_cast<uint32_t>(S >> P.s_shift), P.inv32);
+      unsigned long long r = S - mad_wide(q, static_cast<uint32_t>(p), 0ull) - (static_cast<unsigned long long>(q * static_cast<uint32_t>(p >> 32)) << 32);
+      r = r >= p ? r - p : r;
+      sm = r >= p ? r - p : r;
     } else {
       const unsigned long long lo = a[0] + (static_cast<unsigned long long>(a[1]) << 8) +
                                     (static_cast<unsigned long long>(a[2]) << 16) +
@@ -405,9 +429,18 @@ __device__ __forceinline__ void crt_step(const CrtParams& P, int c, i64 colh, do
                                     (static_cast<unsigned long long>(a[6]) << 16);  // < 2^37
       sm = barrett(dev::shoup_mulmod(hi, P.two32, P.two32_sh, p) + lo, p, P.mu);
     }
-    // t M mod p: for n <= 16, t < 2^12 and t (M mod p) < 2^64 is one u64
-    const unsigned long long tmod = P.nmod <= 16 ? barrett(static_cast<unsigned long long>(tt) * P.Mp, p, P.mu)
-                                                 : dev::shoup_mulmod(tt, P.Mp, P.Mp_sh, p);
+    // t M mod p: t < 2^12 (n <= 16), a 32-bit Shoup product leaves [0, 2p)
+    unsigned long long tmod;
+    if (P.nmod <= 16) {
+      const uint32_t qt = __umulhi(tt, P.Mp_sh32);
+      const unsigned long long tm = mad_wide(tt, static_cast<uint32_t>(P.Mp), 0ull) +
+                                    (static_cast<unsigned long long>(tt * static_cast<uint32_t>(P.Mp >> 32)) << 32) -
+                                    mad_wide(qt, static_cast<uint32_t>(p), 0ull) -
+                                    (static_cast<unsigned long long>(qt * static_cast<uint32_t>(p >> 32)) << 32);
+      tmod = tm >= p ? tm - p : tm;
+    } else {
+      tmod = dev::shoup_mulmod(tt, P.Mp, P.Mp_sh, p);
+    }
     const unsigned long long r = sm >= tmod ? sm - tmod : sm + p - tmod;
     out[e] = __longlong_as_double(static_cast<long long>(r | 0x4330000000000000ull)) - 4503599627370496.0;
   }
