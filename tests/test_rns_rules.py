@@ -175,3 +175,30 @@ def test_default_engine_choice(shape, bits, want):
     """The measured winner at each BASELINE config (profiles/round1/configs.json)."""
     m, k, n = shape
     assert F.select_engine(m, k, n, F.prev_prime(1 << bits)) == want
+
+
+def test_crt_final_quotient_estimate_bound():
+    """rns_crt_kernel (n <= 16): q = umulhi(S >> s, floor(2^(s+32)/p)) with
+    s = max(0, bits(p) - 20) is floor(S/p) - {0, 1, 2} for every S <= 16 * 255 *
+    (p - 1), so two conditional subtracts finish S mod p; and the 32-bit Shoup
+    product t (M mod p) lands in [0, 2p) for t < 2^12."""
+    import random
+    rnd = random.Random(3)
+    for bits in range(3, 53):
+        p = F.prev_prime(1 << bits)
+        if p < 5:
+            continue
+        b = (p - 1).bit_length()  # ceil(log2 p), as the host's loop computes it
+        s = max(0, b - 20)
+        inv = (1 << (s + 32)) // p
+        assert inv < 1 << 32 and (1 << s) < p
+        smax = 16 * 255 * (p - 1)
+        assert smax >> s < 1 << 32
+        for S in [0, 1, p - 1, p, smax, smax - 1] + [rnd.randrange(smax + 1) for _ in range(300)]:
+            q = ((S >> s) * inv) >> 32
+            assert 0 <= S // p - q <= 2, (bits, S)
+        Mp = rnd.randrange(p)
+        w = (Mp << 32) // p
+        for t in [0, 1, 4095] + [rnd.randrange(4096) for _ in range(50)]:
+            qt = (t * w) >> 32
+            assert 0 <= t * Mp - qt * p < 2 * p
