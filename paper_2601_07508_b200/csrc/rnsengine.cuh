@@ -83,6 +83,7 @@ struct Params {
   int splits;
   int group;         // pair-tile rows per rasterisation group
   int small_t;       // seg_kb * kBK * 255^2 < 2^24: products reduce without the 16-bit split
+  int flat;          // PassIter order (see there)
   unsigned epi_sleep_ns;  // epilogue's accumulator wait: sleep between polls (ns), 0 = suspending try_wait
   i64 split_stride;
   unsigned long long p, mu;            // Barrett: mu = floor(2^64 / p)
@@ -559,6 +560,27 @@ __device__ __forceinline__ void commit_pair(uint64_t* bar) {
       : "memory");
 }
 
+// The pair's work items (modulus i, item t) in order.  flat: one sequence
+// over i * total + t, so every pair runs the same number of items (+-1) and
+// the pairs that share a wave's panels stay in lockstep across moduli;
+// otherwise each modulus restarts at t = pair (pairs with one item fewer per
+// modulus run ahead into the next modulus).
+struct PassIter {
+  int i, t;
+  __device__ __forceinline__ PassIter(int pair) : i(0), t(pair) {}
+  __device__ __forceinline__ void next(const Params& P, int pair, int npairs, int total) {
+    if (P.flat) {
+      const int g = i * total + t + npairs;
+      i = g / total;
+      t = g - i * total;
+    } else {
+      t += npairs;
+      if (t >= total) ++i, t = pair;
+    }
+  }
+  __device__ __forceinline__ bool valid(const Params& P, int total) const { return i < P.nmod && t < total; }
+};
+
 // The pair (cluster of 2 CTAs on neighbouring SMs) computes a 256 x 256 tile:
 // CTA r holds rows 128 r.. of A and columns 128 r.. of B in its shared
 // memory and rows 128 r.. of the accumulator in its TMEM; the leader (r = 0)
@@ -608,8 +630,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
       // (measured and rejected: L2 evict_last/evict_first hints for A/B, -2..10%;
       // cp.async.bulk.prefetch.L2 8..64 k-blocks ahead, -9..19%)
       int g = 0;
-      for (int i = 0; i < P.nmod; ++i) {
-        for (int t = pair; t < total; t += npairs) {
+      for (PassIter pi(pair); pi.valid(P, total); pi.next(P, pair, npairs, total)) {
+        {
+          const int i = pi.i, t = pi.t;
           const Item it = item_of(t, P);
           const int kb0 = it.ks * P.kb_per_split;
           const int nkb = max(0, min(P.KB, kb0 + P.kb_per_split) - kb0);
@@ -631,8 +654,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
       // ---------------- MMA issuer (leader CTA, one thread) ----------------
       constexpr uint32_t idesc = i8::instr_desc(kPairM, kNT);
       int g = 0, pass = 0;
-      for (int i = 0; i < P.nmod; ++i) {
-        for (int t = pair; t < total; t += npairs) {
+      for (PassIter pi(pair); pi.valid(P, total); pi.next(P, pair, npairs, total)) {
+        {
+          const int t = pi.t;
           const Item it = item_of(t, P);
           const int kb0 = it.ks * P.kb_per_split;
           const int nkb = max(0, min(P.KB, kb0 + P.kb_per_split) - kb0);
@@ -676,9 +700,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
     const uint32_t tlane = static_cast<uint32_t>(quad * 32) << 16;
     const uint32_t leader_tmem_empty = peer_addr(tmem_empty, 0);
     int pass = 0;
-    for (int i = 0; i < P.nmod; ++i) {
+    for (PassIter pi(pair); pi.valid(P, total); pi.next(P, pair, npairs, total)) {
+      const int i = pi.i, t = pi.t;
       const uint32_t m = P.mod[i], nm = P.negm[i], c16 = P.c16[i], mg = P.magic[i];
-      for (int t = pair; t < total; t += npairs) {
+      {
         const Item it = item_of(t, P);
         const int kb0 = it.ks * P.kb_per_split;
         const int nkb = max(0, min(P.KB, kb0 + P.kb_per_split) - kb0);
