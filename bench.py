@@ -372,8 +372,9 @@ def main():
         F.ENGINE_DMMA: "mwgemm_kernel: DMMA.8x8x4 FP64 tensor pipe; work = 2uv*mnk FP64 flops",
         F.ENGINE_I8: "mwi8_kernel: tcgen05.mma.kind::i8 (UTCIMMA), TMEM int32; work = 2*D^2*mnk int8 tensor "
                      "ops (D base-256 digits)",
-        F.ENGINE_RNS: "rns_kernel: tcgen05.mma.cta_group::2.kind::i8 (UTCIMMA.2CTA) M256 N256, TMEM int32, fused "
-                      "CRT epilogue; work = 2*n_mod*mnk int8 tensor ops (n_mod byte moduli)",
+        F.ENGINE_RNS: "rns_kernel: tcgen05.mma.cta_group::2.kind::i8 (UTCIMMA.2CTA) M256 N256, TMEM int32; the "
+                      "epilogue parks T_i mod m_i (rns_crt_kernel rebuilds C); work = 2*n_mod*mnk int8 tensor ops "
+                      "(n_mod byte moduli)",
     }
     for eng in ("auto", "i8", "rns", "dmma"):
         rec = {}
