@@ -60,6 +60,12 @@ typedef enum {
  * use other word counts where the caller's collapse the exact K-block
  * (lambda_k = 4 at the rule's limits, e.g. (2,2) at 52 bits); C is the same. */
 #define FPMM_B200_DMMA_EXACT_WORDS 0x80u
+/* Instrumented mode, the analogue of the reference's shadow replay
+ * (shadow.hpp:125-162, `fpmm check --checked`): the FP64 engine verifies at
+ * every in-register reduction (and before its epilogue) that each accumulator
+ * is at most 2^53 in magnitude, i.e. still exact; a violation fails the call
+ * with FPMM_B200_ECONTRACT.  The int8 engines are exact by construction. */
+#define FPMM_B200_CHECK_EXACTNESS 0x200u
 
 /* product variants (multiword.hpp:113-254); all map to the same fused kernel */
 typedef enum {

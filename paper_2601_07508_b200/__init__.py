@@ -74,6 +74,7 @@ ENGINE_I8 = 0x20    # base-256 multiword on tcgen05.mma.kind::i8 (TMEM int32 acc
 ENGINE_RNS = 0x40   # byte residues mod coprime m_i <= 256, one kind::i8 GEMM per modulus, fused CRT
 DMMA_EXACT_WORDS = 0x80  # FP64 engine: exactly the caller's (u,v) words (default may pick cheaper counts)
 ASYNC = 0x100
+CHECK_EXACTNESS = 0x200  # FP64 engine: verify every accumulator <= 2^53 at each reduction (shadow-replay analogue)
 PLAIN, WORKSPACE, CONCAT = 0, 1, 2
 _ENGINE_MASK = ENGINE_DMMA | ENGINE_I8 | ENGINE_RNS
 _default_engine_flags = 0

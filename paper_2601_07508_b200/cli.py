@@ -5,6 +5,9 @@
         [--scale S] [--bits 20 26 ...] [--variant u,v|auto ...] [--lambda auto|N]
         [--kernel b200|b200-rns|b200-i8|b200-dmma|b200-dmma-exact] [--runs R] [--seed S] [--out CSV]
         [--extended] [--device-resident]
+  python -m paper_2601_07508_b200.cli check [--bits ...] [--dims m,k,n ...] [--variant u,v ...]
+        [--op plain|concat|workspace] [--seed S] [--seeds N] [--kernel ...] [--lambda N] [--checked]
+        [--trials T] [--dump-dir DIR] [--quiet]
   python -m paper_2601_07508_b200.cli crossover bench.csv [--out CSV]
   python -m paper_2601_07508_b200.cli plan --bits B [--dims m,k,n] [--min-lambda L]
 
@@ -15,7 +18,13 @@ block size, both decompositions and the product are inside the timer; for
 the unbalanced scenario A's words are prepared once outside it.  Inputs are
 host matrices (the drop-in's calling convention), so the timer also covers
 the PCIe transfers.  ``crossover`` reproduces crossover_table
-(bench.cpp:93-136).  Exit codes follow the reference: 0 ok, 1 failure,
+(bench.cpp:93-136).  ``check`` is the oracle-equivalence suite of
+run_check (driver.cpp:37-140, defaults driver.hpp:21-33) with PASS/FAIL/SKIP
+lines (fpmm_cli.cpp:52-66).  It verifies C without recomputing it on the CPU:
+exact Freivalds trials (C s == A (B s) mod p in Python integers) plus sampled
+entries, each an exact dot product, which name the first mismatching
+position.  ``--checked`` (the reference's shadow replay) turns on
+CHECK_EXACTNESS; ``--dump-dir`` writes a failing case's A and B as .npy.  Exit codes follow the reference: 0 ok, 1 failure,
 2 usage error (fpmm_cli.cpp:14-16).
 """
 from __future__ import annotations
@@ -28,7 +37,8 @@ import time
 
 import numpy as np
 
-from . import (DMMA_EXACT_WORDS, ENGINE_DMMA, ENGINE_I8, ENGINE_RNS, Error, FpContext, InfeasibleError, Timing, kVariants,
+from . import (CHECK_EXACTNESS, DMMA_EXACT_WORDS, ENGINE_DMMA, ENGINE_I8, ENGINE_RNS, Error, FpContext, InfeasibleError,
+               Timing, kVariants, mw_product, mw_product_concat, mw_product_workspace, variant_bit_limit,
                matrix_seed, mw_block_size, plan_for_modulus, prev_prime, random_mat,
                variant_admits_bits)
 
@@ -232,6 +242,96 @@ def crossover_table(rows):
     return out
 
 
+# ------------------------------------------------------------------- check
+CHECK_DIMS = [(17, 33, 9), (64, 64, 64), (128, 300, 32)]
+CHECK_BITS = [5, 20, 26, 30, 35, 39, 42, 48, 52]
+ORACLE_CAP = 512
+
+
+def verify_product(A, B, C, p: int, trials: int, samples: int, seed: int):
+    """None if C == A B mod p passes `trials` exact Freivalds trials and the
+    sampled entries, else a note naming the failure.  Exact Python-integer
+    arithmetic; C itself is never recomputed."""
+    m, k = A.shape
+    n = B.shape[1]
+    if m == 0 or n == 0:
+        return None
+    rng = np.random.default_rng(seed)
+    Ai = A.astype(np.int64)
+    Bi = B.astype(np.int64)
+    Ci = C.astype(np.int64)
+    if (Ci < 0).any() or (Ci >= p).any():
+        i, j = np.argwhere((Ci < 0) | (Ci >= p))[0]
+        return "entry (%d,%d) = %d outside [0, p)" % (i, j, Ci[i, j])
+    for (i, j) in zip(rng.integers(0, m, samples), rng.integers(0, n, samples)):
+        want = sum(int(Ai[i, t]) * int(Bi[t, j]) for t in range(k)) % p
+        if int(Ci[i, j]) != want:
+            return "mismatch at (%d,%d): got %d, want %d" % (i, j, int(Ci[i, j]), want)
+    Ao, Bo, Co = Ai.astype(object), Bi.astype(object), Ci.astype(object)
+    for t in range(trials):
+        sv = np.array([int(x) for x in rng.integers(0, p, n, dtype=np.int64)], dtype=object)
+        lhs = Co.dot(sv) % p
+        rhs = Ao.dot(Bo.dot(sv) % p) % p
+        if not (lhs == rhs).all():
+            return "Freivalds trial %d failed (row %d)" % (t, int(np.argmax(lhs != rhs)))
+    return None
+
+
+def run_check(args):
+    """driver.cpp:37-140: every variant x bitsize x shape x seed against an
+    independent check; the planned lambda unless --lambda overrides it."""
+    dims = [parse_dims(d) for d in args.dims] if args.dims else CHECK_DIMS
+    for d in dims:
+        if max(d) > ORACLE_CAP:
+            raise Error("check: dims exceed the oracle cap of %d" % ORACLE_CAP)
+    variants = parse_variants(args.variant) or [(v.u, v.v) for v in kVariants]
+    product = {"plain": mw_product, "concat": mw_product_concat, "workspace": mw_product_workspace}[args.op]
+    flags = KERNELS[args.kernel] | (CHECK_EXACTNESS if args.checked else 0)
+    passed = failed = skipped = 0
+    lines = []
+    for (m, k, n) in dims:
+        for bits in args.bits:
+            for s in range(args.seeds):
+                seed = args.seed + s
+                p = prev_prime(1 << bits) if 2 <= bits <= 52 else 0
+                problem = ""
+                if bits > 52:
+                    problem = "modulus unrepresentable at t=53"
+                elif p < 5 or p.bit_length() != bits:
+                    problem = "no usable prime of bitsize %d" % bits
+                A = B = None
+                for (u, v) in variants:
+                    label = "(%d,%d) bits=%d dims=%dx%dx%d seed=%d" % (u, v, bits, m, k, n, seed)
+                    status, note = "SKIP", problem
+                    if not problem and bits > variant_bit_limit(u, v):
+                        note = "skipped (over variant bit limit %d)" % variant_bit_limit(u, v)
+                    elif not problem:
+                        if A is None:
+                            A = random_mat(m, k, p, matrix_seed(seed, bits, m, k, n, 0xA))
+                            B = random_mat(k, n, p, matrix_seed(seed, bits, m, k, n, 0xB))
+                        lam = args.lambda_ if args.lambda_ else min(mw_block_size(u, v, p), max(k, 1))
+                        try:
+                            C = product(A, B, u, v, lam, FpContext.make(p), flags=flags)
+                            bad = verify_product(A, B, C, p, args.trials, 4, seed * 1000003 + bits)
+                            status, note = ("FAIL", bad) if bad else ("PASS", "")
+                            if bad and args.dump_dir:
+                                import os
+                                os.makedirs(args.dump_dir, exist_ok=True)
+                                np.save(os.path.join(args.dump_dir, "fail_A.npy"), A)
+                                np.save(os.path.join(args.dump_dir, "fail_B.npy"), B)
+                        except InfeasibleError as e:
+                            status, note = ("FAIL" if args.lambda_ else "SKIP"), str(e)
+                        except Error as e:  # e.g. the CHECK_EXACTNESS contract
+                            status, note = "FAIL", str(e)
+                    passed += status == "PASS"
+                    failed += status == "FAIL"
+                    skipped += status == "SKIP"
+                    if not args.quiet or status == "FAIL":
+                        lines.append("%s  %s: %s" % (status, label, note))
+    lines.append("check: %d passed, %d failed, %d skipped" % (passed, failed, skipped))
+    return failed, lines
+
+
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="fpmm-b200", description="exact modular matrix multiplication on B200")
     sub = ap.add_subparsers(dest="cmd", required=True)
@@ -249,6 +349,19 @@ def main(argv=None) -> int:
     b.add_argument("--extended", action="store_true")
     b.add_argument("--device-resident", action="store_true",
                    help="square scenario with inputs already on the GPU, timed by CUDA events (no PCIe)")
+    ck = sub.add_parser("check", help="oracle-equivalence suite (PASS/FAIL/SKIP per case)")
+    ck.add_argument("--bits", type=int, nargs="+", default=CHECK_BITS)
+    ck.add_argument("--dims", nargs="+")
+    ck.add_argument("--variant", nargs="+", default=["auto"])
+    ck.add_argument("--op", default="plain", choices=["plain", "concat", "workspace"])
+    ck.add_argument("--seed", type=int, default=1)
+    ck.add_argument("--seeds", type=int, default=3)
+    ck.add_argument("--kernel", default="b200", choices=sorted(KERNELS))
+    ck.add_argument("--lambda", dest="lambda_", type=int, default=0)
+    ck.add_argument("--checked", action="store_true")
+    ck.add_argument("--trials", type=int, default=2)
+    ck.add_argument("--dump-dir")
+    ck.add_argument("--quiet", action="store_true")
     c = sub.add_parser("crossover", help="best-variant bitsize intervals from a bench CSV")
     c.add_argument("csv")
     c.add_argument("--out")
@@ -268,6 +381,10 @@ def main(argv=None) -> int:
                     write_csv(rows, f, args.extended)
             else:
                 write_csv(rows, sys.stdout, args.extended)
+        elif args.cmd == "check":
+            failed, lines = run_check(args)
+            print("\n".join(lines))
+            return 1 if failed else 0
         elif args.cmd == "crossover":
             table = crossover_table(read_csv(args.csv))
             buf = io.StringIO()

@@ -759,12 +759,14 @@ int launch_gemm_rns(const Job& j, const void* apack, const void* bpack, double* 
 // `mid` (nullable) is recorded after the product kernel, before any
 // reconstruction kernel (RNS CRT, int8 split-K combine).
 int launch_gemm(const Job& j, const void* apack_v, const void* bpack_v, double* C, i64 ldc, i64 rows,
-                cudaStream_t s, Workspace& ws, cudaEvent_t mid = nullptr) {
+                cudaStream_t s, Workspace& ws, cudaEvent_t mid = nullptr, int* overflow = nullptr) {
   if (j.engine == kRns) return launch_gemm_rns(j, apack_v, bpack_v, C, ldc, rows, s, mid, ws);
   if (j.engine == kI8) return launch_gemm_i8(j, apack_v, bpack_v, C, ldc, rows, s, mid, ws);
   const double* apack = static_cast<const double*>(apack_v);
   const double* bpack = static_cast<const double*>(bpack_v);
   GemmParams g = j.gp;
+  g.overflow = overflow;  // CHECK_EXACTNESS (FP64 engine only: the int8 engines are exact by construction)
+  if (const char* e = std::getenv("FPMM_B200_TEST_RED_EVERY")) g.red_every = std::max(1, std::atoi(e));
   g.apack = apack;
   g.bpack = bpack;
   g.C = C;
@@ -800,7 +802,9 @@ void check_err_flag(DeviceCtx& c, cudaStream_t s) {
   int h = 0;
   CUDA_OK(cudaMemcpyAsync(&h, c.err.ptr, sizeof(int), cudaMemcpyDeviceToHost, s));
   CUDA_OK(cudaStreamSynchronize(s));
-  if (h) throw Failure(FPMM_B200_ECONTRACT, "multiword product: inputs must be residues in [0, p)");
+  if (h & 1) throw Failure(FPMM_B200_ECONTRACT, "multiword product: inputs must be residues in [0, p)");
+  if (h & 2)
+    throw Failure(FPMM_B200_ECONTRACT, "exactness check: an FP64 accumulator exceeded 2^53 before its reduction");
 }
 
 // Zero the rows x n block of C (k == 0 product).
@@ -858,15 +862,17 @@ void product_device(const ProductArgs& a, int device, void* stream, fpmm_b200_ti
   void* apack = ws.apack.get(j.apack_bytes);
   void* bpack = ws.bpack.get(j.bpack_bytes);
   int* err = nullptr;
-  if (a.flags & FPMM_B200_CHECK_INPUTS) {
+  if (a.flags & (FPMM_B200_CHECK_INPUTS | FPMM_B200_CHECK_EXACTNESS)) {
     err = static_cast<int*>(c.err.get(sizeof(int)));
     CUDA_OK(cudaMemsetAsync(err, 0, sizeof(int), s));
   }
+  int* err_in = (a.flags & FPMM_B200_CHECK_INPUTS) ? err : nullptr;
   if (tm) CUDA_OK(cudaEventRecord(c.ev[0], s));
-  launch_pack_a(j, a.A, a.lda, a.m, apack, err, s);
-  launch_pack_b(j, a.B, a.ldb, bpack, err, s);
+  launch_pack_a(j, a.A, a.lda, a.m, apack, err_in, s);
+  launch_pack_b(j, a.B, a.ldb, bpack, err_in, s);
   if (tm) CUDA_OK(cudaEventRecord(c.ev[1], s));
-  const int gl = launch_gemm(j, apack, bpack, a.C, a.ldc, a.m, s, ws, tm ? c.ev[5] : nullptr);
+  const int gl = launch_gemm(j, apack, bpack, a.C, a.ldc, a.m, s, ws, tm ? c.ev[5] : nullptr,
+                             (a.flags & FPMM_B200_CHECK_EXACTNESS) ? err : nullptr);
   if (tm) CUDA_OK(cudaEventRecord(c.ev[2], s));
   if (err) check_err_flag(c, s);
   if (tm) {
@@ -956,14 +962,15 @@ void product_prepared_device(const Prepared* h, const double* dB, i64 ldb, doubl
   Workspace& ws = c.ws_for(s);
   void* bpack = ws.bpack.get(j.bpack_bytes);
   int* err = nullptr;
-  if (fl & FPMM_B200_CHECK_INPUTS) {
+  if (fl & (FPMM_B200_CHECK_INPUTS | FPMM_B200_CHECK_EXACTNESS)) {
     err = static_cast<int*>(c.err.get(sizeof(int)));
     CUDA_OK(cudaMemsetAsync(err, 0, sizeof(int), s));
   }
   if (tm) CUDA_OK(cudaEventRecord(c.ev[0], s));
-  launch_pack_b(j, dB, ldb, bpack, err, s);
+  launch_pack_b(j, dB, ldb, bpack, (fl & FPMM_B200_CHECK_INPUTS) ? err : nullptr, s);
   if (tm) CUDA_OK(cudaEventRecord(c.ev[1], s));
-  const int gl = launch_gemm(j, h->words.ptr, bpack, dC, ldc, h->m, s, ws, tm ? c.ev[5] : nullptr);
+  const int gl = launch_gemm(j, h->words.ptr, bpack, dC, ldc, h->m, s, ws, tm ? c.ev[5] : nullptr,
+                             (fl & FPMM_B200_CHECK_EXACTNESS) ? err : nullptr);
   if (tm) CUDA_OK(cudaEventRecord(c.ev[2], s));
   if (err) check_err_flag(c, s);
   if (tm) {
@@ -1025,7 +1032,7 @@ void product_host(const ProductArgs& a, int ngpus, fpmm_b200_timing* tm) {
   }
   const Job j = make_job(a.m, a.k, a.n, a.p, a.u, a.v, resolve_engine(a.flags),
                      (a.flags & FPMM_B200_DMMA_EXACT_WORDS) != 0);
-  const unsigned chk = a.flags & FPMM_B200_CHECK_INPUTS;
+  const unsigned chk = a.flags & (FPMM_B200_CHECK_INPUTS | FPMM_B200_CHECK_EXACTNESS);
 
   if (ngpus == 1) {
     // Three-stream pipeline over row chunks of A / C: H2D of chunk i+1 and
@@ -1068,14 +1075,16 @@ void product_host(const ProductArgs& a, int ngpus, fpmm_b200_timing* tm) {
     }
     CUDA_OK(cudaStreamWaitEvent(s, c.ev[1], 0));
     CUDA_OK(cudaEventRecord(c.ev[2], s));
-    launch_pack_b(j, dB, a.n, bpack, err, s);
+    int* err_in = (a.flags & FPMM_B200_CHECK_INPUTS) ? err : nullptr;
+    int* err_ex = (a.flags & FPMM_B200_CHECK_EXACTNESS) ? err : nullptr;
+    launch_pack_b(j, dB, a.n, bpack, err_in, s);
     int nl = 1;
     for (int i = 0; i < nch; ++i) {
       const i64 r0 = i * chunk_rows, rn = std::min<i64>(a.m - r0, chunk_rows);
       uint8_t* ap = apack + static_cast<size_t>(r0 / j.BM) * per_rb;
       CUDA_OK(cudaStreamWaitEvent(s, c.ev_in[i], 0));
-      launch_pack_a(j, dA + r0 * a.k, a.k, rn, ap, err, s);
-      nl += 1 + launch_gemm(j, ap, bpack, dC + r0 * a.n, a.n, rn, s, c.ws0);
+      launch_pack_a(j, dA + r0 * a.k, a.k, rn, ap, err_in, s);
+      nl += 1 + launch_gemm(j, ap, bpack, dC + r0 * a.n, a.n, rn, s, c.ws0, nullptr, err_ex);
       CUDA_OK(cudaEventRecord(c.ev_out[i], s));
       CUDA_OK(cudaStreamWaitEvent(so, c.ev_out[i], 0));
       CUDA_OK(cudaMemcpy2DAsync(a.C + r0 * a.ldc, a.ldc * 8, dC + r0 * a.n, a.n * 8, a.n * 8, rn,
@@ -1112,7 +1121,7 @@ void product_host(const ProductArgs& a, int ngpus, fpmm_b200_timing* tm) {
   for (int g = 0; g < ngpus; ++g) cs[g] = &ctx(g);
   std::vector<double*> dA(ngpus), dC(ngpus);
   std::vector<void*> apack(ngpus), bpack(ngpus);
-  std::vector<int*> errs(ngpus, nullptr);
+  std::vector<int*> errs(ngpus, nullptr), errs_in(ngpus, nullptr), errs_ex(ngpus, nullptr);
   double* dB0 = nullptr;
   for (int g = 0; g < ngpus; ++g) {
     DeviceCtx& c = *cs[g];
@@ -1124,6 +1133,8 @@ void product_host(const ProductArgs& a, int ngpus, fpmm_b200_timing* tm) {
     if (chk) {
       errs[g] = static_cast<int*>(c.err.get(sizeof(int)));
       CUDA_OK(cudaMemsetAsync(errs[g], 0, sizeof(int), c.stream));
+      if (a.flags & FPMM_B200_CHECK_INPUTS) errs_in[g] = errs[g];
+      if (a.flags & FPMM_B200_CHECK_EXACTNESS) errs_ex[g] = errs[g];
     }
     CUDA_OK(cudaEventRecord(c.ev[0], c.stream));
     if (rn[g] > 0)
@@ -1134,8 +1145,8 @@ void product_host(const ProductArgs& a, int ngpus, fpmm_b200_timing* tm) {
       CUDA_OK(cudaMemcpy2DAsync(dB0, a.n * 8, a.B, a.ldb * 8, a.n * 8, a.k, cudaMemcpyHostToDevice, c.stream));
     }
     CUDA_OK(cudaEventRecord(c.ev[1], c.stream));
-    if (rn[g] > 0) launch_pack_a(j, dA[g], a.k, rn[g], apack[g], errs[g], c.stream);
-    if (g == 0 && !raw) launch_pack_b(j, dB0, a.n, bpack[0], errs[0], c.stream);
+    if (rn[g] > 0) launch_pack_a(j, dA[g], a.k, rn[g], apack[g], errs_in[g], c.stream);
+    if (g == 0 && !raw) launch_pack_b(j, dB0, a.n, bpack[0], errs_in[0], c.stream);
     CUDA_OK(cudaEventRecord(c.ev[2], c.stream));
   }
   // B crosses NVLink once, as packed words or (fewer bytes / BCAST_RAW_B) as raw residues packed per device
@@ -1158,14 +1169,14 @@ void product_host(const ProductArgs& a, int ngpus, fpmm_b200_timing* tm) {
   if (raw)
     for (int g = 0; g < ngpus; ++g) {
       CUDA_OK(cudaSetDevice(g));
-      launch_pack_b(j, dBg[g], a.n, bpack[g], g == 0 ? errs[0] : nullptr, cs[g]->stream);
+      launch_pack_b(j, dBg[g], a.n, bpack[g], g == 0 ? errs_in[0] : nullptr, cs[g]->stream);
     }
   int nl = raw ? ngpus : 1;
   for (int g = 0; g < ngpus; ++g) {
     DeviceCtx& c = *cs[g];
     CUDA_OK(cudaSetDevice(g));
     CUDA_OK(cudaEventRecord(c.ev[3], c.stream));
-    if (rn[g] > 0) nl += 1 + launch_gemm(j, apack[g], bpack[g], dC[g], a.n, rn[g], c.stream, c.ws0);
+    if (rn[g] > 0) nl += 1 + launch_gemm(j, apack[g], bpack[g], dC[g], a.n, rn[g], c.stream, c.ws0, nullptr, errs_ex[g]);
     CUDA_OK(cudaEventRecord(c.ev[4], c.stream));
     if (rn[g] > 0)
       CUDA_OK(cudaMemcpy2DAsync(a.C + r0[g] * a.ldc, a.ldc * 8, dC[g], a.n * 8, a.n * 8, rn[g],
@@ -1496,11 +1507,13 @@ void dist_product_device(const double* dA_rows, i64 lda, const double* dB, i64 l
   Workspace& ws = c.ws_for(s);
   void* apack = ws.apack.get(j.apack_bytes);
   void* bpack = ws.bpack.get(j.bpack_bytes);
-  int* err = nullptr;
-  if (flags & FPMM_B200_CHECK_INPUTS) {
-    err = static_cast<int*>(c.err.get(sizeof(int)));
-    CUDA_OK(cudaMemsetAsync(err, 0, sizeof(int), s));
+  int* errbuf = nullptr;
+  if (flags & (FPMM_B200_CHECK_INPUTS | FPMM_B200_CHECK_EXACTNESS)) {
+    errbuf = static_cast<int*>(c.err.get(sizeof(int)));
+    CUDA_OK(cudaMemsetAsync(errbuf, 0, sizeof(int), s));
   }
+  int* err = (flags & FPMM_B200_CHECK_INPUTS) ? errbuf : nullptr;
+  int* err_ex = (flags & FPMM_B200_CHECK_EXACTNESS) ? errbuf : nullptr;
   CUDA_OK(cudaEventRecord(c.ev[0], s));
   // B crosses NVLink once: as packed words, or as raw residues (8 B per
   // element) packed by every rank when that is fewer bytes (the RNS engine
@@ -1557,7 +1570,7 @@ void dist_product_device(const double* dA_rows, i64 lda, const double* dB, i64 l
     const i64 o = mine[ci].first, l = mine[ci].second;
     if (l <= 0) continue;
     gl += launch_gemm(j, static_cast<uint8_t*>(apack) + static_cast<size_t>(o / j.BM) * j.per_rb_bytes, bpack,
-                      dC_rows + o * ldc, ldc, l, s, ws);
+                      dC_rows + o * ldc, ldc, l, s, ws, nullptr, err_ex);
     if (dC_full) CUDA_OK(cudaEventRecord(c.ev_out[ci], s));
   }
   CUDA_OK(cudaEventRecord(c.ev[3], s));
@@ -1604,7 +1617,7 @@ void dist_product_device(const double* dA_rows, i64 lda, const double* dB, i64 l
     CUDA_OK(cudaStreamWaitEvent(s, c.ev[5], 0));  // the call completes on its own stream
   }
   CUDA_OK(cudaEventRecord(c.ev[4], s));
-  if (err) check_err_flag(c, s);
+  if (errbuf) check_err_flag(c, s);
   if (!(flags & FPMM_B200_ASYNC) || tm) CUDA_OK(cudaStreamSynchronize(s));
   if (tm) {
     tm->pack_ms = elapsed(c.ev[0], c.ev[1]);

@@ -164,9 +164,30 @@ struct GemmParams {
   int MB, NB, KB;
   int red_every;   // k4-steps between in-register reductions (lambda_k / 4)
   double pf, q;    // p, fl(1/p)
+  int* overflow;   // CHECK_EXACTNESS: |accumulator| > 2^53 seen before a reduction -> *overflow |= 2
   unsigned long long p;
   unsigned long long gamma[kMaxPairs], gamma_sh[kMaxPairs];  // alpha^i beta^j mod p, Shoup consts
 };
+
+// Instrumented mode (the reference's shadow replay, shadow.hpp:125-162, run by
+// `fpmm check --checked`): every accumulator must be an exact integer of
+// magnitude <= 2^53 when it is reduced, i.e. no DMMA partial sum left the
+// exactly representable range.  One flag word per call; off unless asked.
+template <int U, int V, int MT, int NT>
+__device__ __forceinline__ void check_exact(const double (&acc)[U][V][MT][NT][2], int* flag) {
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < U; ++i)
+#pragma unroll
+    for (int j = 0; j < V; ++j)
+#pragma unroll
+      for (int a = 0; a < MT; ++a)
+#pragma unroll
+        for (int b = 0; b < NT; ++b)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) bad |= fabs(acc[i][j][a][b][e]) > 9007199254740992.0;
+  if (bad) atomicOr(flag, 2);
+}
 
 template <int U, int V, int MT, int NT>
 __global__ void __launch_bounds__(256, 1) mwgemm_kernel(const __grid_constant__ GemmParams P) {
@@ -257,6 +278,7 @@ __global__ void __launch_bounds__(256, 1) mwgemm_kernel(const __grid_constant__ 
             for (int b = 0; b < NT; ++b) dev::dmma884(acc[i][j][a][b][0], acc[i][j][a][b][1], fa[i][a], fb[j][b]);
       if (++cnt == P.red_every) {
         cnt = 0;
+        if (P.overflow) check_exact<U, V, MT, NT>(acc, P.overflow);
 #pragma unroll
         for (int i = 0; i < U; ++i)
 #pragma unroll
@@ -286,6 +308,7 @@ __global__ void __launch_bounds__(256, 1) mwgemm_kernel(const __grid_constant__ 
   }
 
   // (3) epilogue: canonical residues of every pair, gamma-weighted sum mod p
+  if (P.overflow) check_exact<U, V, MT, NT>(acc, P.overflow);
   const unsigned long long p = P.p;
   const i64 row_base = static_cast<i64>(tm) * BM + wm * MT * 8 + lane / 4;
   const i64 col_base = static_cast<i64>(tn) * BN + wn * NT * 8 + 2 * (lane % 4);

@@ -50,3 +50,36 @@ def test_bench_csv_on_gpu(tmp_path):
     assert status[(27, 1, 1)] == "infeasible" and status[(26, 1, 1)] == "ok"
     assert cli.main(["bench", "--scenario", "unbalanced", "--scale", "0.05", "--bits", "40", "--runs", "1",
                      "--out", str(tmp_path / "u.csv")]) == 0
+
+
+def test_check_verifier_catches_wrong_products():
+    """cli.verify_product (the check suite's verifier: exact Freivalds trials
+    plus sampled exact entries) accepts the oracle's C and rejects C with one
+    corrupted entry or an entry outside [0, p)."""
+    import numpy as np
+
+    import oracle as O
+    from paper_2601_07508_b200 import cli
+    p, A, B = O.seeded_inputs(40, 70, 30, 48)
+    C = O.exact_mod_gemm(A, B, p)
+    assert cli.verify_product(A, B, C, p, 2, 4, 7) is None
+    bad = C.copy()
+    bad[13, 17] = (bad[13, 17] + 1) % p
+    assert cli.verify_product(A, B, bad, p, 2, 4, 7) is not None
+    bad = C.copy()
+    bad[0, 0] = float(p)
+    assert "outside" in cli.verify_product(A, B, bad, p, 2, 4, 7)
+    assert cli.verify_product(np.zeros((0, 5)), np.zeros((5, 3)), np.zeros((0, 3)), p, 2, 4, 7) is None
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kernel,extra", [("b200", []), ("b200-dmma-exact", ["--checked"]), ("b200-rns", ["--op", "workspace"])])
+def test_check_suite_on_gpu(capsys, kernel, extra):
+    """`check` (driver.cpp:37-140): the standard suite's shapes at a subset of
+    bitsizes passes on every engine; one line per case, then the summary."""
+    from paper_2601_07508_b200 import cli
+    rc = cli.main(["check", "--bits", "5", "26", "39", "52", "--seeds", "1", "--kernel", kernel] + extra)
+    out = capsys.readouterr().out
+    assert rc == 0, out
+    assert "FAIL" not in out and "check: " in out and " 0 failed" in out
+    assert out.count("PASS") >= 12

@@ -336,3 +336,28 @@ def test_dmma_reduction_extremes(engine, bits, u, v):
         for fl in (0, F.DMMA_EXACT_WORDS):
             C = F.mw_product(A, B, u, v, ref_lambda(u, v, p, k), F.FpContext.make(p), flags=fl)
             assert (C == want).all(), (bits, u, v, fl)
+
+
+@pytest.mark.parametrize("bits,u,v", [(52, 2, 2), (50, 2, 2), (39, 1, 3), (26, 1, 1)])
+def test_check_exactness_mode(engine, monkeypatch, bits, u, v):
+    """CHECK_EXACTNESS (the reference's `check --checked` shadow replay): on
+    inputs that maximise the balanced words (floor(p/2), the largest centred
+    magnitude) every accumulator stays <= 2^53 at its reduction, so the
+    checked product passes; with the reduction period forced past the exact
+    K-block (test hook) the check fails the call with ContractError instead
+    of returning a wrong C."""
+    if engine != "dmma":
+        pytest.skip("FP64 engine only (the int8 engines are exact by construction)")
+    p = F.prev_prime(1 << bits)
+    h = p // 2
+    m, k, n = 64, 4096, 40
+    A = np.full((m, k), float(h))
+    B = np.full((k, n), float(h))
+    lam = ref_lambda(u, v, p, k)
+    want = (k * h * h) % p
+    for fl in (0, F.DMMA_EXACT_WORDS):
+        C = F.mw_product(A, B, u, v, lam, F.FpContext.make(p), flags=fl | F.CHECK_EXACTNESS)
+        assert (C == want).all()
+    monkeypatch.setenv("FPMM_B200_TEST_RED_EVERY", str(k // 4))  # one reduction for the whole K
+    with pytest.raises(F.ContractError):
+        F.mw_product(A, B, u, v, lam, F.FpContext.make(p), flags=F.DMMA_EXACT_WORDS | F.CHECK_EXACTNESS)
