@@ -640,7 +640,7 @@ int launch_gemm_i8(const Job& j, const void* apack, const void* bpack, double* C
 }
 
 // 2-D uint8 tensor map over `bytes` of a packed operand viewed as 128-byte
-// rows, box 128 x 64 (one 8 KB chunk); the encoder comes from the driver
+// rows, box 128 x (stage chunk / 128); the encoder comes from the driver
 // through the runtime (no libcuda link dependency).
 CUtensorMap chunk_map(const void* base, size_t bytes) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
@@ -653,9 +653,11 @@ CUtensorMap chunk_map(const void* base, size_t bytes) {
     encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
   CUtensorMap m{};
-  const cuuint64_t dims[2] = {128, std::max<cuuint64_t>(64, bytes / 128)};
+  constexpr cuuint32_t kRows = rns::kAStage / 128;  // one stage chunk (kBStage == kAStage)
+  static_assert(rns::kAStage == rns::kBStage, "A and B stage chunks share the tensor-map box");
+  const cuuint64_t dims[2] = {128, std::max<cuuint64_t>(kRows, bytes / 128)};
   const cuuint64_t strides[1] = {128};
-  const cuuint32_t box[2] = {128, 64};
+  const cuuint32_t box[2] = {128, kRows};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,

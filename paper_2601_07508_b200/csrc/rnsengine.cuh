@@ -49,12 +49,17 @@ constexpr int kBM = 128;             // rows per CTA (each CTA's half of the pai
 constexpr int kNT = 256;             // columns per tile (MMA N)
 constexpr int kBH = kNT / 2;         // B columns held by each CTA of the pair
 constexpr int kPairM = 2 * kBM;      // rows per pair tile
-constexpr int kBK = 64;              // k bytes per pipeline stage
+// k bytes per pipeline stage: 128 (four K=32 MMAs per stage barrier) ran the
+// 8192^3 residue GEMMs 9% faster than 64 (two); 256 was within 1.5% of 128
+#ifndef FPMM_B200_RNS_BK
+#define FPMM_B200_RNS_BK 128
+#endif
+constexpr int kBK = FPMM_B200_RNS_BK;
 constexpr int kKSteps = kBK / 32;    // MMA K = 32 for kind::i8
-constexpr int kAStage = kBM * kBK;   // 8 KB: this CTA's 128 rows of A
-constexpr int kBStage = kBH * kBK;   // 8 KB: this CTA's 128 columns of B
+constexpr int kAStage = kBM * kBK;   // this CTA's 128 rows of A (16 KB)
+constexpr int kBStage = kBH * kBK;   // this CTA's 128 columns of B (16 KB)
 constexpr int kStageBytes = kAStage + kBStage;
-constexpr int kStages = 12;
+constexpr int kStages = 12 * 64 / kBK;  // 192 KB of stages
 #ifndef FPMM_B200_RNS_EPI_WARPS
 #define FPMM_B200_RNS_EPI_WARPS 8
 #endif
@@ -62,6 +67,7 @@ constexpr int kEpiWarps = FPMM_B200_RNS_EPI_WARPS;  // 8 or 16: 4 TMEM lane quad
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kEpiCols = 4 * kNT / kEpiWarps;        // accumulator columns per epilogue warp
 static_assert(kEpiWarps == 8 || kEpiWarps == 16, "epilogue warps");
+static_assert(kBK % 64 == 0 && kBK <= 256, "stage k-depth: 64, 128 or 256 bytes");
 constexpr int kSmem = kStages * kStageBytes + 1024;
 constexpr int kSlotPerMod = kBM * kNT;  // scratch bytes per modulus per CTA tile (32 KB)
 constexpr int kGroup = 16;              // pair-tile rows per rasterisation group
@@ -69,7 +75,7 @@ constexpr int kGroup = 16;              // pair-tile rows per rasterisation grou
 // Per-modulus constants (host: rns_plan in rules.cpp).
 struct Params {
   // 2-D byte views (128-byte rows) of the packed operands for the pair TMA
-  // loads; a chunk of 8 KB is one 128 x 64 box at row 64 * chunk
+  // loads; a chunk of kAStage bytes is one 128 x (kAStage / 128) box
   CUtensorMap tmA, tmB;
   const uint8_t* apack;  // [128-row block][modulus][k-block] chunks of kAStage bytes
   const uint8_t* bpack;  // [128-column block][modulus][k-block] chunks of kBStage bytes
@@ -207,30 +213,37 @@ __global__ void __launch_bounds__(256) pack_a_rns(const double* __restrict__ A, 
 __global__ void __launch_bounds__(128) pack_b_rns(const double* __restrict__ B, i64 ldb, i64 k, i64 n, int KB,
                                                   int NB128, int kb_begin, int kb_count,
                                                   const __grid_constant__ PackParams P, uint8_t* __restrict__ out) {
-  constexpr int SW = 32, SUB = kBH / SW;
-  __shared__ double tile[kBK][SW + 1];
-  const i64 tiles = static_cast<i64>(kb_count) * NB128 * SUB;
+  constexpr int SW = 32, SUB = kBH / SW, TK = 64, KSUB = kBK / TK;  // 64 (k) x 32 (column) tiles
+  __shared__ double tile[TK][SW + 1];
+  const i64 tiles = static_cast<i64>(kb_count) * KSUB * NB128 * SUB;
   for (i64 t = blockIdx.x; t < tiles; t += gridDim.x) {
     const int sb = static_cast<int>(t % SUB);
-    const i64 cb = (t / SUB) % NB128, kb = kb_begin + t / (SUB * static_cast<i64>(NB128));
+    const i64 cb = (t / SUB) % NB128, kq = t / (SUB * static_cast<i64>(NB128));
+    const i64 kb = kb_begin + kq / KSUB;
+    const int ks = static_cast<int>(kq % KSUB);  // 64-row slice of the k-block
     __syncthreads();
-    for (int e = threadIdx.x; e < kBK * SW; e += blockDim.x) {
+    for (int e = threadIdx.x; e < TK * SW; e += blockDim.x) {
       const int kr = e / SW, cc = e % SW;
-      const i64 kk = kb * kBK + kr, col = cb * kBH + sb * SW + cc;
+      const i64 kk = kb * kBK + ks * TK + kr, col = cb * kBH + sb * SW + cc;
       tile[kr][cc] = (kk < k && col < n) ? B[kk * ldb + col] : 0.0;
     }
     __syncthreads();
-    const int cc = threadIdx.x % SW, q = threadIdx.x / SW;  // column, k16 chunk
-    double xs[16];
+    const int cc = threadIdx.x % SW;  // column
+    {
+      const int qt = threadIdx.x / SW;     // k16 chunk within the tile
+      const int q = ks * (TK / 16) + qt;   // ... within the k-block
+      double xs[16];
 #pragma unroll
-    for (int e = 0; e < 16; ++e) xs[e] = tile[q * 16 + e][cc];
-    uint32_t lo[16], hi[16];
-    digits16(xs, P.half_p, lo, hi);
-    const int nn = sb * SW + cc, g = nn / 8, r8 = nn % 8;
-    uint8_t* base = out + ((cb * P.nmod) * KB + kb) * static_cast<i64>(kBStage) + ((q * (kBH / 8) + g) * 8 + r8) * 16;
+      for (int e = 0; e < 16; ++e) xs[e] = tile[qt * 16 + e][cc];
+      uint32_t lo[16], hi[16];
+      digits16(xs, P.half_p, lo, hi);
+      const int nn = sb * SW + cc, g = nn / 8, r8 = nn % 8;
+      uint8_t* base =
+          out + ((cb * P.nmod) * KB + kb) * static_cast<i64>(kBStage) + ((q * (kBH / 8) + g) * 8 + r8) * 16;
 #pragma unroll 1
-    for (int i = 0; i < P.nmod; ++i)
-      *reinterpret_cast<uint4*>(base + static_cast<i64>(i) * KB * kBStage) = residues16(lo, hi, P, i);
+      for (int i = 0; i < P.nmod; ++i)
+        *reinterpret_cast<uint4*>(base + static_cast<i64>(i) * KB * kBStage) = residues16(lo, hi, P, i);
+    }
   }
 }
 
@@ -540,7 +553,7 @@ __device__ __forceinline__ void mma_i8_pair(uint32_t tmem_d, uint64_t adesc, uin
       "}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(z));
 }
-// Pair TMA load of one 8 KB chunk (row `row` of the 128-byte view) into this
+// Pair TMA load of one stage chunk (row `row` of the 128-byte view) into this
 // CTA's shared memory, completing on the LEADER's barrier at the same offset
 // (peer bit cleared), so the leader's one barrier tracks both halves.
 __device__ __forceinline__ void tma_pair_load(void* dst, const CUtensorMap* map, int row, uint64_t* bar) {
@@ -585,7 +598,8 @@ struct PassIter {
 // CTA r holds rows 128 r.. of A and columns 128 r.. of B in its shared
 // memory and rows 128 r.. of the accumulator in its TMEM; the leader (r = 0)
 // issues M=256 N=256 K=32 cta_group::2 MMAs that read both halves.  Each SM
-// so streams 8 KB of A and 8 KB of B per 128-cycle k-step (64 B/clk).
+// so streams 4 KB of A and 4 KB of B per 128-cycle K=32 step (64 B/clk); a
+// stage holds kBK / 32 such steps.
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_kernel(const __grid_constant__ Params P) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;
