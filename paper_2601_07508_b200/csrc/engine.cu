@@ -409,7 +409,17 @@ Job make_rns_job(i64 m, i64 k, i64 n, u64 p) {
   }
   rns::PackParams& pp = j.rpp;
   pp.half_p = static_cast<double>(p / 2);
+  pp.pf = static_cast<double>(p);
   pp.nmod = j.nmod;
+  // residues of modulus pairs on the FP64 pipe: packs 5-7% faster at 36-52 bits than the dp4a digit form
+  pp.fp64_pairs = 1;
+  if (const char* e = std::getenv("FPMM_B200_RNS_PACK_FP64")) pp.fp64_pairs = std::atoi(e) != 0;
+  for (int jj = 0; 2 * jj < j.nmod; ++jj) {
+    const u64 L = static_cast<u64>(pl.mod[2 * jj]) * (2 * jj + 1 < j.nmod ? pl.mod[2 * jj + 1] : 1);
+    pp.L[jj] = static_cast<double>(L);
+    pp.invL[jj] = 1.0 / static_cast<double>(L);
+    pp.offL[jj] = 4503599627370496.0 + static_cast<double>(L);
+  }
   for (int i = 0; i < j.nmod; ++i) {
     const u64 mi = pl.mod[i];
     q.mod[i] = pp.mod[i] = static_cast<uint32_t>(mi);

@@ -105,7 +105,10 @@ struct Params {
 
 struct PackParams {
   double half_p;  // floor(p/2): x > half_p is centred to x - p
+  double pf;      // p
   int nmod;
+  int fp64_pairs;  // residues of modulus pairs from x' mod (m_a m_b) on the FP64 pipe (residues16_pair)
+  double L[kMaxMod / 2], invL[kMaxMod / 2], offL[kMaxMod / 2];  // m_2j m_2j+1 (or m_2j alone), fl(1/L), 2^52 + L
   uint32_t mod[kMaxMod];
   uint32_t wlo[kMaxMod];    // bytes (256^j mod m), j = 0..3
   uint32_t whi[kMaxMod];    // bytes (256^j mod m), j = 4..6, and (m - p mod m) mod m in byte 3
@@ -158,6 +161,64 @@ __device__ __forceinline__ uint4 residues16(const uint32_t (&lo)[16], const uint
   return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
+// The residues of moduli 2j and 2j+1 from the centred values xc (exact,
+// |xc| <= p/2 < 2^51): y = xc - rint(xc fl(1/L)) L with L = m_2j m_2j+1 < 2^16
+// is exact and |y| < L/2 + 1 (the quotient estimate is within 2^-16 of xc/L),
+// the low word of y + 2^52 + L is u = y + L in [0, 2L), and u mod m_2j, u mod
+// m_2j+1 are two mod_small each.  Four FP64-pipe ops per pair and two IMADs
+// per residue, against two dp4a and two IMADs per residue on the FMA-heavy
+// pipe for the digit form; centred values need no more registers than digits.
+__device__ __forceinline__ void residues16_pair(const double (&xc)[16], const PackParams& P, int j, uint4& out0,
+                                                uint4& out1) {
+  const double M = 6755399441055744.0;  // 1.5 * 2^52
+  const double L = P.L[j], inv = P.invL[j], off = P.offL[j];
+  const int i0 = 2 * j, i1 = min(2 * j + 1, P.nmod - 1);
+  const uint32_t n0 = P.negm[i0], g0 = P.magic[i0], n1 = P.negm[i1], g1 = P.magic[i1];
+  uint32_t r0[16], r1[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const double q = __fma_rn(xc[e], inv, M) - M;
+    const double y = __fma_rn(-q, L, xc[e]);
+    const uint32_t u = static_cast<uint32_t>(__double2loint(y + off));
+    r0[e] = mod_small(u, n0, g0);
+    r1[e] = mod_small(u, n1, g1);
+  }
+  uint32_t w0[4], w1[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    w0[q] = pack4(r0[4 * q], r0[4 * q + 1], r0[4 * q + 2], r0[4 * q + 3]);
+    w1[q] = pack4(r1[4 * q], r1[4 * q + 1], r1[4 * q + 2], r1[4 * q + 3]);
+  }
+  out0 = make_uint4(w0[0], w0[1], w0[2], w0[3]);
+  out1 = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+}
+
+__device__ __forceinline__ void centre16(const double (&xs)[16], const PackParams& P, double (&xc)[16]) {
+#pragma unroll
+  for (int e = 0; e < 16; ++e) xc[e] = xs[e] > P.half_p ? xs[e] - P.pf : xs[e];
+}
+
+// Every residue plane of one 16-element k row: out + i * plane for modulus i.
+__device__ __forceinline__ void store_residue_planes(const double (&xs)[16], const PackParams& P, uint8_t* out,
+                                                     i64 plane) {
+  if (P.fp64_pairs) {
+    double xc[16];
+    centre16(xs, P, xc);
+#pragma unroll 1
+    for (int j = 0; 2 * j < P.nmod; ++j) {
+      uint4 a, b;
+      residues16_pair(xc, P, j, a, b);
+      *reinterpret_cast<uint4*>(out + (2 * j) * plane) = a;
+      if (2 * j + 1 < P.nmod) *reinterpret_cast<uint4*>(out + (2 * j + 1) * plane) = b;
+    }
+  } else {
+    uint32_t lo[16], hi[16];
+    digits16(xs, P.half_p, lo, hi);
+#pragma unroll 1
+    for (int i = 0; i < P.nmod; ++i) *reinterpret_cast<uint4*>(out + i * plane) = residues16(lo, hi, P, i);
+  }
+}
+
 // A: m x k residues -> N residue planes in the canonical K-major core-matrix
 // layout.  Chunk (rb, i, kb), kAStage bytes: [k16 c (4)][row group g (16)][row (8)][16 B].
 // Thread (row, 16-element k chunk): reads 16 doubles, writes N x 16 bytes.
@@ -194,14 +255,10 @@ __global__ void __launch_bounds__(256) pack_a_rns(const double* __restrict__ A, 
 #pragma unroll
       for (int e = 0; e < 16; ++e) xs[e] = 0.0;
     }
-    uint32_t lo[16], hi[16];
-    digits16(xs, P.half_p, lo, hi);
     const i64 rb = row / kBM, kb = kc / (kBK / 16);
     const int c = static_cast<int>(kc % (kBK / 16)), g = static_cast<int>((row % kBM) / 8);
     uint8_t* base = out + ((rb * P.nmod) * KB + kb) * static_cast<i64>(kAStage) + ((c * (kBM / 8) + g) * 8 + r8) * 16;
-#pragma unroll 1
-    for (int i = 0; i < P.nmod; ++i)
-      *reinterpret_cast<uint4*>(base + static_cast<i64>(i) * KB * kAStage) = residues16(lo, hi, P, i);
+    store_residue_planes(xs, P, base, static_cast<i64>(KB) * kAStage);
   }
 }
 
@@ -235,14 +292,10 @@ __global__ void __launch_bounds__(128) pack_b_rns(const double* __restrict__ B, 
       double xs[16];
 #pragma unroll
       for (int e = 0; e < 16; ++e) xs[e] = tile[qt * 16 + e][cc];
-      uint32_t lo[16], hi[16];
-      digits16(xs, P.half_p, lo, hi);
       const int nn = sb * SW + cc, g = nn / 8, r8 = nn % 8;
       uint8_t* base =
           out + ((cb * P.nmod) * KB + kb) * static_cast<i64>(kBStage) + ((q * (kBH / 8) + g) * 8 + r8) * 16;
-#pragma unroll 1
-      for (int i = 0; i < P.nmod; ++i)
-        *reinterpret_cast<uint4*>(base + static_cast<i64>(i) * KB * kBStage) = residues16(lo, hi, P, i);
+      store_residue_planes(xs, P, base, static_cast<i64>(KB) * kBStage);
     }
   }
 }
