@@ -300,6 +300,38 @@ __global__ void __launch_bounds__(128) pack_b_rns(const double* __restrict__ B, 
   }
 }
 
+// The same packing without the shared-memory transpose: thread (k16 chunk,
+// column) reads its 16 k values straight from B, consecutive threads walking
+// consecutive columns, so each of the 16 loads of a warp is 256 contiguous
+// bytes of one row of B; the stores are pack_a_rns's.
+__global__ void __launch_bounds__(256) pack_b_rns_direct(const double* __restrict__ B, i64 ldb, i64 k, i64 n, int KB,
+                                                         int NB128, int kb_begin, int kb_count,
+                                                         const __grid_constant__ PackParams P,
+                                                         uint8_t* __restrict__ out) {
+  const i64 npad = static_cast<i64>(NB128) * kBH;
+  const i64 chunks = static_cast<i64>(kb_count) * (kBK / 16);
+  const i64 total = chunks * npad;
+  for (i64 idx = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 col = idx % npad;
+    const i64 kc = static_cast<i64>(kb_begin) * (kBK / 16) + idx / npad;  // global k16 chunk
+    const i64 k0 = kc * 16;
+    double xs[16];
+    if (col < n) {
+      const double* src = B + k0 * ldb + col;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) xs[e] = k0 + e < k ? __ldg(src + e * ldb) : 0.0;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) xs[e] = 0.0;
+    }
+    const i64 cb = col / kBH, kb = kc / (kBK / 16);
+    const int q = static_cast<int>(kc % (kBK / 16)), nn = static_cast<int>(col % kBH), g = nn / 8, r8 = nn % 8;
+    uint8_t* base = out + ((cb * P.nmod) * KB + kb) * static_cast<i64>(kBStage) + ((q * (kBH / 8) + g) * 8 + r8) * 16;
+    store_residue_planes(xs, P, base, static_cast<i64>(KB) * kBStage);
+  }
+}
+
 // ------------------------------------------------------------------ GEMM
 // Work item t (0 <= t < MB * NB * splits) -> pair tile (tm, tn), split ks;
 // grouped rasterisation keeps a wave's panels of one modulus in L2.
