@@ -557,10 +557,8 @@ void launch_pack_b_rns(const Job& j, const double* B, i64 ldb, void* bpack, int*
   const i64 r0 = static_cast<i64>(kb0) * rns::kBK, r1 = std::min<i64>(j.k, static_cast<i64>(kb0 + nkb) * rns::kBK);
   if (err && r1 > r0 && j.n > 0)
     check_residues_kernel<<<grid_for((r1 - r0) * j.n, 256), 256, 0, s>>>(B + r0 * ldb, ldb, r1 - r0, j.n, j.p, err);
-  static const bool direct = [] {
-    const char* e = std::getenv("FPMM_B200_RNS_PACKB_SMEM");
-    return !(e && std::atoi(e) != 0);
-  }();
+  const char* smem_env = std::getenv("FPMM_B200_RNS_PACKB_SMEM");
+  const bool direct = !(smem_env && std::atoi(smem_env) != 0);
   if (direct) {
     const i64 items = static_cast<i64>(nkb) * (rns::kBK / 16) * (2 * j.NB) * rns::kBH;
     rns::pack_b_rns_direct<<<grid_for(items, 256), 256, 0, s>>>(B, ldb, j.k, j.n, j.KB, 2 * j.NB, kb0, nkb, j.rpp,

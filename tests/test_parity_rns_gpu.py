@@ -188,3 +188,23 @@ def test_rns_short_k_extremes(bits, k):
     for A, B in cases:
         C = F.mw_product(A, B, pl.u, pl.v, min(pl.lambda_, k), F.FpContext.make(p), flags=RNS)
         assert (C == O.exact_mod_gemm(A, B, p)).all(), (bits, k)
+
+
+@pytest.mark.parametrize("knob,value", [("FPMM_B200_RNS_FLAT", "0"), ("FPMM_B200_RNS_PACK_FP64", "0"),
+                                        ("FPMM_B200_RNS_PACKB_SMEM", "1"), ("FPMM_B200_RNS_EPI_SLEEP", "256"),
+                                        ("FPMM_B200_RNS_GROUP", "3")])
+def test_rns_tuning_knobs_same_c(monkeypatch, knob, value):
+    """Every INTEGRATION.md tuning knob only changes the schedule or the
+    instruction mix: C stays bit-identical to the default's (and to the oracle)."""
+    rng = np.random.default_rng(11)
+    for bits, (m, k, n) in ((52, (700, 900, 600)), (21, (300, 200, 520)), (40, (256, 70, 300))):
+        p = F.prev_prime(1 << bits)
+        A = rng.integers(0, p, size=(m, k)).astype(np.float64)
+        B = rng.integers(0, p, size=(k, n)).astype(np.float64)
+        pl = F.plan_for_modulus(p, m, k, n)
+        ref = F.mw_product(A, B, pl.u, pl.v, min(pl.lambda_, k), F.FpContext.make(p), flags=RNS)
+        monkeypatch.setenv(knob, value)
+        C = F.mw_product(A, B, pl.u, pl.v, min(pl.lambda_, k), F.FpContext.make(p), flags=RNS)
+        monkeypatch.delenv(knob)
+        assert (C == ref).all(), (knob, bits)
+        assert O.freivalds(A, B, C, p, trials=2) == 0
