@@ -361,3 +361,33 @@ def test_check_exactness_mode(engine, monkeypatch, bits, u, v):
     monkeypatch.setenv("FPMM_B200_TEST_RED_EVERY", str(k // 4))  # one reduction for the whole K
     with pytest.raises(F.ContractError):
         F.mw_product(A, B, u, v, lam, F.FpContext.make(p), flags=F.DMMA_EXACT_WORDS | F.CHECK_EXACTNESS)
+
+
+def test_cuda_graph_capture(engine):
+    """The ASYNC device entry is stream-ordered with no host synchronisation,
+    so after one warm-up call (which sizes the workspaces) a product can be
+    captured in a CUDA graph and replayed: bit-identical C."""
+    import torch
+    m = k = n = 512
+    p = F.prev_prime(1 << 50)
+    pl = F.plan_for_modulus(p, m, k, n)
+    A = torch.empty((m, k), dtype=torch.float64, device="cuda")
+    B = torch.empty((k, n), dtype=torch.float64, device="cuda")
+    C = torch.empty((m, n), dtype=torch.float64, device="cuda")
+    F.random_residues_device(A, p, 3)
+    F.random_residues_device(B, p, 4)
+    fl = F.ASYNC  # the fixture's default engine is added by the library binding
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        F.mw_product_device(A, B, C, p, pl.u, pl.v, pl.lambda_, stream=s, flags=fl)
+    torch.cuda.synchronize()
+    ref = C.clone()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        F.mw_product_device(A, B, C, p, pl.u, pl.v, pl.lambda_, stream=s, flags=fl)
+    C.zero_()
+    torch.cuda.synchronize()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(C, ref)
+    assert O.freivalds(A.cpu().numpy(), B.cpu().numpy(), C.cpu().numpy(), p, trials=2) == 0
