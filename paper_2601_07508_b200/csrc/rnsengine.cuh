@@ -50,7 +50,8 @@ constexpr int kNT = 256;             // columns per tile (MMA N)
 constexpr int kBH = kNT / 2;         // B columns held by each CTA of the pair
 constexpr int kPairM = 2 * kBM;      // rows per pair tile
 // k bytes per pipeline stage: 128 (four K=32 MMAs per stage barrier) ran the
-// 8192^3 residue GEMMs 9% faster than 64 (two); 256 was within 1.5% of 128
+// 8192^3 residue GEMMs 9% faster than 64 (two); 256 (three 64 KB stages) was
+// ~1% faster again on the timed sweep, kept off for the deeper pipeline
 #ifndef FPMM_B200_RNS_BK
 #define FPMM_B200_RNS_BK 128
 #endif
