@@ -101,3 +101,34 @@ def test_dist_world1_chunked_gather(engine, shape, bits):
         D.finalize()
     finally:
         td.destroy_process_group()
+
+
+def test_dist_world1_pipelined_bcast_checks_inputs():
+    """CHECK_INPUTS through the pipelined raw-B broadcast (RNS, B >= 256 MB):
+    a non-residue in the last k-chunk of B fails the call with ContractError;
+    CHECK_EXACTNESS on the same call path is accepted (RNS: nothing to check)."""
+    import torch
+    import torch.distributed as td
+    from paper_2601_07508_b200 import dist as D
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()))
+    td.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        D.init_from_torch(0)
+        m, k, n, bits = 512, 4100, 8192, 52
+        p = F.prev_prime(1 << bits)
+        pl = F.plan_for_modulus(p, m, k, n)
+        dA = torch.empty((m, k), dtype=torch.float64, device="cuda")
+        dB = torch.empty((k, n), dtype=torch.float64, device="cuda")
+        F.random_residues_device(dA, p, 5)
+        F.random_residues_device(dB, p, 6)
+        dCr = torch.empty((m, n), dtype=torch.float64, device="cuda")
+        dCf = torch.empty((m, n), dtype=torch.float64, device="cuda")
+        D.mw_product_device(dA, dB, dCr, p, pl.u, pl.v, pl.lambda_, m, root=0, C_full=dCf,
+                            flags=F.ENGINE_RNS | F.CHECK_INPUTS | F.CHECK_EXACTNESS)
+        dB[k - 1, n - 1] = float(p)
+        with pytest.raises(F.ContractError):
+            D.mw_product_device(dA, dB, dCr, p, pl.u, pl.v, pl.lambda_, m, root=0, C_full=dCf,
+                                flags=F.ENGINE_RNS | F.CHECK_INPUTS)
+        D.finalize()
+    finally:
+        td.destroy_process_group()
