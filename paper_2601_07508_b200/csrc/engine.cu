@@ -715,8 +715,29 @@ int launch_gemm_rns_rows(const Job& j, const void* apack, const void* bpack, dou
   CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const i64 items = static_cast<i64>(q.MB) * q.NB * splits;
   if (items > 0x7fffffff) throw Failure(FPMM_B200_EERROR, "problem too large for one launch");
-  // persistent CTA pairs (clusters of 2 on neighbouring SMs)
-  const unsigned grid = 2 * static_cast<unsigned>(std::max<i64>(1, std::min<i64>(items, sms / 2)));
+  // persistent CTA pairs (clusters of 2 on neighbouring SMs): no more pairs
+  // than can be co-resident (a GPC with an odd SM count leaves one SM out of
+  // every pair), so no pair waits for another to finish
+  static int max_pairs[64] = {};
+  if (!max_pairs[dev & 63]) {
+    CUDA_OK(cudaFuncSetAttribute(rns::rns_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, rns::kSmem));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(sms / 2 * 2));
+    cfg.blockDim = dim3(rns::kThreads);
+    cfg.dynamicSmemBytes = rns::kSmem;
+    cudaLaunchAttribute attr{};
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = 2, attr.val.clusterDim.y = 1, attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int clusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&clusters, rns::rns_kernel, &cfg) != cudaSuccess || clusters < 1) {
+      cudaGetLastError();
+      clusters = sms / 2;
+    }
+    max_pairs[dev & 63] = std::min(clusters, sms / 2);
+  }
+  const unsigned grid = 2 * static_cast<unsigned>(std::max<i64>(1, std::min<i64>(items, max_pairs[dev & 63])));
   // residue bytes of every item: n bytes per output element and slice
   q.scratch = static_cast<uint8_t*>(ws.scratch.get(static_cast<size_t>(items) * 2 * j.nmod * rns::kSlotPerMod));
   q.group = rns::kGroup;
