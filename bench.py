@@ -425,6 +425,34 @@ def main():
         if pk == "i8":
             engines[eng]["roofline"]["frac_of_burst_peak"] = round(achieved / peaks["i8_burst"], 4)
     roof = dict(engines[args.engine]["roofline"])
+    # HBM rooflines of the RNS engine's memory-side kernels over the sweep
+    # (north star: achieved HBM GB/s of the decomposition): the packs read 8 B
+    # and write n_mod B per operand element; the CRT reads n_mod B and writes
+    # 8 B per output element.  Times are the library's CUDA events around them.
+    hbm_peak = None
+    try:
+        hbm_peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        pass
+    memside = {}
+    rs = engines["rns"]["sweep"]
+    pk_b = pk_t = cr_b = cr_t = 0.0
+    for (b, p, u, v, lam, lk) in probs:
+        e = rs[str(b)]
+        nm = e.get("moduli", 0)
+        rn = rows[b][1]
+        pk_b += (8.0 + nm) * (rn * k + k * n)
+        pk_t += e["pack_ms"]
+        cr_b += (nm + 8.0) * rn * n
+        cr_t += e["recon_ms"]
+    for key, by, t, kern in (("decomposition", pk_b, pk_t, "pack_a_rns + pack_b_rns_direct (A and B residue planes)"),
+                             ("reconstruction", cr_b, cr_t, "rns_crt_kernel (parked residues -> C)")):
+        if t > 0:
+            gbs = by / (t * 1e-3) / 1e9
+            memside[key] = {"kernel": kern, "bound": "hbm", "achieved": round(gbs, 1), "peak": hbm_peak,
+                            "unit": "GB/s", "frac": round(gbs / hbm_peak, 4) if hbm_peak else None,
+                            "bytes_per_step": int(by), "ms_per_step": round(t, 3),
+                            "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, read + write)"}
     # end to end through the public host-buffer API (pinned memory), one step
     e2e = None
     if not args.no_e2e:
@@ -461,6 +489,7 @@ def main():
             "engine": args.engine,
             "roofline": roof,
             "fp64_uv_frac": engines["dmma"]["roofline"]["frac"],
+            "memory_side": memside,
             "engines": engines,
             "e2e": e2e,
             "cpu_baseline": cpu,
