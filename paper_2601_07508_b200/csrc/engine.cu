@@ -80,8 +80,8 @@ struct DevBuf {
 // different sets, so independent products overlap on the device (the packs
 // and reconstruction of one run beside the tensor-core kernel of another).
 struct Workspace {
-  DevBuf apack, bpack, scratch, splitws;
-  void release() { apack.release(), bpack.release(), scratch.release(), splitws.release(); }
+  DevBuf apack, bpack, scratch, splitws, rawb;  // rawb: the partitioner's broadcast copy of raw B
+  void release() { apack.release(), bpack.release(), scratch.release(), splitws.release(), rawb.release(); }
 };
 
 struct DeviceCtx {
@@ -1565,9 +1565,12 @@ void dist_product_device(const double* dA_rows, i64 lda, const double* dB, i64 l
   // pack of B (about 9 ms at 32768^2) hides under the broadcast.
   const int bchunks = (raw && j.engine == kRns && static_cast<size_t>(8) * k * n >= (size_t{256} << 20))
                           ? std::min(4, j.KB) : 1;
+  // Every NCCL call of the partitioner goes to the device's s_out stream, in
+  // the same program order on every rank, so products issued on different
+  // caller streams never run collectives of the one communicator concurrently.
+  cudaStream_t so = c.s_out;
   if (raw && bchunks > 1) {
-    cudaStream_t so = c.s_out;
-    double* dBd = static_cast<double*>(c.b.get(sizeof(double) * k * n));
+    double* dBd = static_cast<double*>(ws.rawb.get(sizeof(double) * k * n));
     if (g_dist.rank == root)
       CUDA_OK(cudaMemcpy2DAsync(dBd, n * 8, dB, ldb * 8, n * 8, k, cudaMemcpyDeviceToDevice, s));
     CUDA_OK(cudaEventRecord(c.ev[6], s));  // B staged; the last call's reads of dBd are done
@@ -1586,18 +1589,24 @@ void dist_product_device(const double* dA_rows, i64 lda, const double* dB, i64 l
       launch_pack_b_rns(j, dBd, n, bpack, g_dist.rank == root ? err : nullptr, s, kb0, nkb);
     }
   } else if (raw) {
-    double* dBd = static_cast<double*>(c.b.get(sizeof(double) * k * n));
+    double* dBd = static_cast<double*>(ws.rawb.get(sizeof(double) * k * n));
     if (g_dist.rank == root)
       CUDA_OK(cudaMemcpy2DAsync(dBd, n * 8, dB, ldb * 8, n * 8, k, cudaMemcpyDeviceToDevice, s));
     if (rn > 0) launch_pack_a(j, dA_rows, lda, rn, apack, err, s);
     CUDA_OK(cudaEventRecord(c.ev[1], s));
-    NCCL_OK(nccl().Broadcast(dBd, dBd, static_cast<size_t>(k * n), ncclDouble, root, g_dist.comm, s));
+    CUDA_OK(cudaStreamWaitEvent(so, c.ev[1], 0));
+    NCCL_OK(nccl().Broadcast(dBd, dBd, static_cast<size_t>(k * n), ncclDouble, root, g_dist.comm, so));
+    CUDA_OK(cudaEventRecord(c.ev[6], so));
+    CUDA_OK(cudaStreamWaitEvent(s, c.ev[6], 0));
     launch_pack_b(j, dBd, n, bpack, g_dist.rank == root ? err : nullptr, s);
   } else {
     if (g_dist.rank == root) launch_pack_b(j, dB, ldb, bpack, err, s);
     if (rn > 0) launch_pack_a(j, dA_rows, lda, rn, apack, err, s);
     CUDA_OK(cudaEventRecord(c.ev[1], s));
-    NCCL_OK(nccl().Broadcast(bpack, bpack, j.bpack_bytes, ncclUint8, root, g_dist.comm, s));
+    CUDA_OK(cudaStreamWaitEvent(so, c.ev[1], 0));
+    NCCL_OK(nccl().Broadcast(bpack, bpack, j.bpack_bytes, ncclUint8, root, g_dist.comm, so));
+    CUDA_OK(cudaEventRecord(c.ev[6], so));
+    CUDA_OK(cudaStreamWaitEvent(s, c.ev[6], 0));
   }
   CUDA_OK(cudaEventRecord(c.ev[2], s));
   // the product in row chunks; with a gather, chunk c's rows travel to root
@@ -1620,7 +1629,6 @@ void dist_product_device(const double* dA_rows, i64 lda, const double* dB, i64 l
     // gather row blocks to root (grouped point-to-point; NCCL has no gather)
     if (ldc != n || (g_dist.rank == root && ldc_full != n))
       throw Failure(FPMM_B200_EERROR, "dist_mw_product: gather needs dense row blocks (ld == n)");
-    cudaStream_t so = c.s_out;
     CUDA_OK(cudaStreamWaitEvent(so, c.ev[2], 0));  // root's copies / recvs follow this call's earlier work
     std::vector<std::vector<std::pair<i64, i64>>> theirs(g_dist.nranks);
     std::vector<i64> q0s(g_dist.nranks, 0);
