@@ -83,3 +83,13 @@ def test_check_suite_on_gpu(capsys, kernel, extra):
     assert rc == 0, out
     assert "FAIL" not in out and "check: " in out and " 0 failed" in out
     assert out.count("PASS") >= 12
+
+
+def test_check_argument_errors(capsys):
+    """check's argument handling needs no GPU: dims over the oracle cap fail
+    with exit code 1 (driver.cpp:44-46), a malformed --dims with 1, usage errors
+    with 2 (fpmm_cli.cpp:14-16)."""
+    assert cli.main(["check", "--dims", "513,4,4"]) == 1
+    assert "oracle cap" in capsys.readouterr().err
+    assert cli.main(["check", "--dims", "4,4"]) == 1
+    assert cli.main(["check", "--op", "nonsense"]) == 2
