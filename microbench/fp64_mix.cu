@@ -21,7 +21,7 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
 constexpr int CH = 8;  // DMMA chains per thread per iteration
 
 // side work kinds (R independent values per iteration)
-enum { kNone = 0, kInt = 1, kF32 = 2, kDfma = 3, kRedClassic = 4, kRedFast = 5, kIntF32 = 6 };
+enum { kNone = 0, kInt = 1, kF32 = 2, kDfma = 3, kRedClassic = 4, kRedFast = 5, kIntF32 = 6, kRedIntQ = 7 };
 
 template <int KIND, int R>
 __device__ __forceinline__ void side(double* x, uint32_t* u, float* f, double p, double q, float qf) {
@@ -40,6 +40,18 @@ __device__ __forceinline__ void side(double* x, uint32_t* u, float* f, double p,
       const double M = 6755399441055744.0;
       const double cq = __fma_rn(x[c], q, M) - M;
       x[c] = __fma_rn(-cq, p, x[c]) + 4.0 * p;  // keeps x large; the DADD is extra
+    } else if constexpr (KIND == kRedIntQ) {
+      // quotient from x's high word with integer ops only (IMAD-class), then
+      // c = (1.5*2^52 + q) - 1.5*2^52 (one DADD) and r = fma(-c, p, x): 2 FP64 ops
+      const uint32_t hi = static_cast<uint32_t>(__double2hiint(x[c]));
+      const uint32_t mant = (hi & 0xFFFFFu) | 0x100000u;          // 21-bit significand
+      const int e = static_cast<int>((hi >> 20) & 0x7FFu) - 1023;  // x in [2^e, 2^(e+1))
+      const uint32_t qq = __umulhi(mant << 11, static_cast<uint32_t>(qf * 4294967296.0f));  // ~ mant * 2^31 / p'
+      const int sh = 31 - e;  // placeholder scaling: the cost, not the value, is what is measured
+      const uint32_t q = sh > 0 && sh < 32 ? (qq >> sh) : qq;
+      const long long qs = (hi >> 31) ? -static_cast<long long>(q) : static_cast<long long>(q);
+      const double cd = __longlong_as_double(0x4338000000000000ll + qs) - 6755399441055744.0;
+      x[c] = __fma_rn(-cd, p, x[c]) + 4.0 * p;
     } else if constexpr (KIND == kRedFast) {
       const uint32_t hi = static_cast<uint32_t>(__double2hiint(x[c]));
       const float fx = __uint_as_float(hi * 8u + 0x40000000u);
@@ -136,5 +148,8 @@ int main(int argc, char** argv) {
   ROW(kRedFast, 4, "+4 fast red (+DADD)")
   ROW(kRedFast, 8, "+8 fast red (+DADD)")
   ROW(kRedFast, 16, "+16 fast red (+DADD)")
+  ROW(kRedIntQ, 4, "+4 int-quotient red (+DADD)")
+  ROW(kRedIntQ, 8, "+8 int-quotient red (+DADD)")
+  ROW(kRedIntQ, 16, "+16 int-quotient red (+DADD)")
   return 0;
 }
