@@ -4,6 +4,8 @@ import os
 import re
 import subprocess
 
+import pytest
+
 import paper_2601_07508_b200 as F
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -56,3 +58,15 @@ def test_cpp_shim_compiles_and_runs_host_rules(tmp_path):
                     F.LIB_PATH, "-Wl,-rpath," + os.path.dirname(F.LIB_PATH)], check=True)
     out = subprocess.run([str(exe)], capture_output=True, text=True, check=True)
     assert "OK" in out.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_shim_product_on_gpu(tmp_path):
+    """A reference-style C++ program against the drop-in header runs every
+    engine and product variant on the GPU and matches exact dot products."""
+    src = os.path.join(ROOT, "tests", "cpp", "shim_product.cpp")
+    exe = tmp_path / "shim_product"
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"), src, "-o", str(exe),
+                    F.LIB_PATH, "-Wl,-rpath," + os.path.dirname(F.LIB_PATH)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and "OK" in out.stdout, out.stdout + out.stderr
