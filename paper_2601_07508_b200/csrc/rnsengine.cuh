@@ -60,7 +60,7 @@ constexpr int kKSteps = kBK / 32;    // MMA K = 32 for kind::i8
 constexpr int kAStage = kBM * kBK;   // this CTA's 128 rows of A (16 KB)
 constexpr int kBStage = kBH * kBK;   // this CTA's 128 columns of B (16 KB)
 constexpr int kStageBytes = kAStage + kBStage;
-constexpr int kStages = 12 * 64 / kBK;  // 192 KB of stages
+constexpr int kStages = 12 * 64 / kBK;  // 192 KB of stages (kBK 64, 128, 192, 256)
 #ifndef FPMM_B200_RNS_EPI_WARPS
 #define FPMM_B200_RNS_EPI_WARPS 8
 #endif
