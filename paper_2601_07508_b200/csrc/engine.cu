@@ -1611,9 +1611,8 @@ void dist_product_device(const double* dA_rows, i64 lda, const double* dB, i64 l
   CUDA_OK(cudaEventRecord(c.ev[2], s));
   // the product in row chunks; with a gather, chunk c's rows travel to root
   // on stream s_out (NCCL P2P) while chunk c+1 computes on s.  Every NCCL call
-  // of this product is issued in the same order on every rank: the broadcast
-  // (stream s, complete before any chunk's compute), then one group per chunk
-  // index on s_out.
+  // of this product is issued on s_out in the same order on every rank: the
+  // broadcast (all of it, or its k-chunks), then one group per chunk index.
   const auto mine = dC_full ? gather_chunks(j, rn) : std::vector<std::pair<i64, i64>>{{0, rn}};
   int gl = 0;
   for (size_t ci = 0; ci < mine.size(); ++ci) {
