@@ -506,8 +506,12 @@ def mw_product_concat_words(da, db, m, k, n, lambda_, F, kernel=None, side="auto
     return _words_product(da, db, m, k, n, lambda_, F, CONCAT, kw.get("flags", 0), kw.get("timing"))
 
 
-def block_gemm_mod(Cm: np.ndarray, A, B, lambda_: int, F: FpContext, kernel=None) -> None:
-    """block_product.hpp:62-73: C <- C + A B mod p in place (C reduced mod p)."""
+def block_gemm_mod(Cm: np.ndarray, A, B, lambda_: int, F: FpContext, kernel=None, *, flags: int = 0) -> None:
+    """block_product.hpp:62-73: C <- C + A B mod p in place (C reduced mod p).
+
+    Operands may exceed p (e.g. words bounded by alpha): the value is the
+    reference's wherever its panel loop is exact.  CHECK_INPUTS enforces the
+    reference's contract (lambda max(A) max(B) + p - 1 <= 2^t, C reduced)."""
     A = _f64(A)
     B = _f64(B)
     if A.shape[0] != Cm.shape[0] or B.shape[1] != Cm.shape[1] or A.shape[1] != B.shape[0]:
@@ -517,7 +521,7 @@ def block_gemm_mod(Cm: np.ndarray, A, B, lambda_: int, F: FpContext, kernel=None
     m, k = A.shape
     n = B.shape[1]
     _check(lib().fpmm_b200_block_gemm_mod(_ptr(Cm), max(n, 1), _ptr(A), _ld(A), _ptr(B), _ld(B), m,
-                                          k, n, lambda_, F.p, 0))
+                                          k, n, lambda_, F.p, _eng(flags)))
 
 
 class GemmKernel:
@@ -555,11 +559,15 @@ def kernel_by_name(name: str) -> Optional[GemmKernel]:
 CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy
 
 
-def _stream_handle(stream):
-    """ctypes value for a torch stream: None -> the library's own stream; the
-    default (legacy) stream, whose handle is 0, -> cudaStreamLegacy."""
+def _stream_handle(stream, device=None):
+    """ctypes value for a torch stream.  None -> torch's current stream on
+    `device`, so a call on torch tensors is ordered after the torch work that
+    produced them (e.g. a non_blocking H2D copy) and before the work that
+    reads its result; the default (legacy) stream, whose handle is 0, ->
+    cudaStreamLegacy."""
     if stream is None:
-        return None
+        import torch
+        stream = torch.cuda.current_stream(device)
     return stream.cuda_stream or CUDA_STREAM_LEGACY
 
 
@@ -580,7 +588,7 @@ def mw_product_device(A, B, Cout, p: int, u: int, v: int, lambda_: int, *, varia
     if allow_composite:
         flags |= ALLOW_COMPOSITE
     dev = A.device.index
-    sp = _stream_handle(stream)
+    sp = _stream_handle(stream, dev)
     _check(lib().fpmm_b200_mw_product_device(A.data_ptr(), _dev_ld(A), B.data_ptr(), _dev_ld(B),
                                              Cout.data_ptr(), _dev_ld(Cout), m, k, n, p, u, v,
                                              lambda_, variant, dev, sp, _eng(flags),
@@ -600,7 +608,7 @@ class PreparedA:
         self.device = A.device.index
         h = C.c_void_p()
         _check(lib().fpmm_b200_prepare_a_device(A.data_ptr(), _dev_ld(A), self.m, self.k, p, u, v,
-                                                _eng(flags), self.device, _stream_handle(stream),
+                                                _eng(flags), self.device, _stream_handle(stream, self.device),
                                                 C.byref(h)))
         self._h = h
 
@@ -612,7 +620,7 @@ class PreparedA:
             raise Error("multiword product: dimension mismatch")
         _check(lib().fpmm_b200_mw_product_prepared_device(
             self._h, B.data_ptr(), _dev_ld(B), Cout.data_ptr(), _dev_ld(Cout), n, lambda_,
-            _stream_handle(stream), flags, C.byref(timing) if timing is not None else None))
+            _stream_handle(stream, self.device), flags, C.byref(timing) if timing is not None else None))
 
     def close(self) -> None:
         if getattr(self, "_h", None) is not None and self._h.value:
@@ -630,7 +638,7 @@ def decompose_device(M, p: int, u: int, words, stream=None) -> int:
     """Reference-identical words of device matrix M into words (u x rows x cols)."""
     rows, cols = M.shape
     base = C.c_uint64()
-    sp = _stream_handle(stream)
+    sp = _stream_handle(stream, M.device.index)
     _check(lib().fpmm_b200_decompose_device(M.data_ptr(), _dev_ld(M), rows, cols, p, u,
                                             words.data_ptr(), rows * cols, C.byref(base),
                                             M.device.index, sp))
@@ -640,7 +648,7 @@ def decompose_device(M, p: int, u: int, words, stream=None) -> int:
 def accumulate_device(Cm, A, B, stream=None) -> None:
     m, w = A.shape
     n = B.shape[1]
-    sp = _stream_handle(stream)
+    sp = _stream_handle(stream, A.device.index)
     _check(lib().fpmm_b200_accumulate_device(Cm.data_ptr(), _dev_ld(Cm), A.data_ptr(), _dev_ld(A),
                                              B.data_ptr(), _dev_ld(B), m, w, n, A.device.index, sp))
 
@@ -648,7 +656,7 @@ def accumulate_device(Cm, A, B, stream=None) -> None:
 def random_residues_device(M, p: int, seed: int, row0: int = 0, stream=None) -> None:
     """Fill device tensor M (rows row0.. of a global matrix) with uniform residues in [0,p)."""
     rows, cols = M.shape
-    sp = _stream_handle(stream)
+    sp = _stream_handle(stream, M.device.index)
     _check(lib().fpmm_b200_random_residues_device(M.data_ptr(), _dev_ld(M), rows, cols, row0, p,
                                                   seed, M.device.index, sp))
 

@@ -18,6 +18,7 @@
 #include "i8engine.cuh"
 #include "kernels.cuh"
 #include "rnsengine.cuh"
+#include "verify.cuh"
 
 namespace fpmm_b200 {
 
@@ -36,7 +37,15 @@ namespace fpmm_b200 {
 
 namespace {
 
-std::recursive_mutex g_mu;
+// Locking.  The context table has its own mutex, held only to look up or
+// create a device's context.  Every call that uses a device holds that
+// device's (recursive) mutex for its duration: host threads driving different
+// GPUs run concurrently, calls on one device serialise (they share its
+// workspaces and events).  Multi-device calls take the device locks in
+// increasing device order; the partitioner's communicator (g_dist_mu) and the
+// in-process communicators (g_all_mu) are locked before any device.
+std::mutex g_ctx_mu;
+std::recursive_mutex g_dist_mu, g_all_mu;
 
 // grow-only device buffer.  A grow is a cudaFree + cudaMalloc that
 // serialises the device (hundreds of ms for GB-sized workspaces), so it
@@ -85,12 +94,13 @@ struct Workspace {
 };
 
 struct DeviceCtx {
+  std::recursive_mutex mu;  // held by every call using this device
   static constexpr int kChunks = 16;  // host-path pipeline depth (exposed head/tail ~1/16 of a product)
   static constexpr int kStreamSets = 8;
   int dev = -1;
   cudaStream_t stream = nullptr, s_in = nullptr, s_out = nullptr;
   cudaEvent_t ev[8] = {}, ev_in[kChunks] = {}, ev_out[kChunks] = {};
-  DevBuf a, b, c, tmp, err;
+  DevBuf a, b, c, tmp, err, ver, agree;
   Workspace ws0;  // the library's own stream and the legacy default stream
   std::vector<std::pair<cudaStream_t, std::unique_ptr<Workspace>>> ws_streams;
   Workspace& ws_for(cudaStream_t s) {
@@ -129,7 +139,7 @@ struct DeviceCtx {
     if (s_in) cudaStreamDestroy(s_in), s_in = nullptr;
     if (s_out) cudaStreamDestroy(s_out), s_out = nullptr;
     if (stream) cudaStreamDestroy(stream), stream = nullptr;
-    a.release(), b.release(), c.release(), tmp.release(), err.release();
+    a.release(), b.release(), c.release(), tmp.release(), err.release(), ver.release(), agree.release();
     ws0.release();
     for (auto& e : ws_streams) e.second->release();
     ws_streams.clear();
@@ -145,14 +155,26 @@ DeviceCtx& ctx(int dev) {
   if (dev < 0 || dev >= count)
     throw Failure(FPMM_B200_EERROR, "device " + std::to_string(dev) + " out of range (" +
                                         std::to_string(count) + " visible)");
-  if (g_ctx.size() < static_cast<size_t>(count)) g_ctx.resize(count);
-  if (!g_ctx[dev]) {
-    g_ctx[dev] = std::make_unique<DeviceCtx>();
-    g_ctx[dev]->init(dev);
+  DeviceCtx* c = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
+    if (g_ctx.size() < static_cast<size_t>(count)) g_ctx.resize(count);
+    if (!g_ctx[dev]) {
+      auto fresh = std::make_unique<DeviceCtx>();
+      fresh->init(dev);
+      g_ctx[dev] = std::move(fresh);
+    }
+    c = g_ctx[dev].get();
   }
   CUDA_OK(cudaSetDevice(dev));
-  return *g_ctx[dev];
+  return *c;
 }
+
+// the calling thread holds device `dev` for the scope (and its context exists)
+struct DevLock {
+  std::unique_lock<std::recursive_mutex> lk;
+  explicit DevLock(int dev) : lk(ctx(dev).mu) { CUDA_OK(cudaSetDevice(dev)); }
+};
 
 // ----------------------------------------------------------- (u,v) dispatch
 // warp tile per word pair: MT x NT DMMA tiles of 8x8 (<= 64 fp64 accumulators)
@@ -661,15 +683,15 @@ int launch_gemm_i8(const Job& j, const void* apack, const void* bpack, double* C
 // rows, box 128 x (stage chunk / 128); the encoder comes from the driver
 // through the runtime (no libcuda link dependency).
 CUtensorMap chunk_map(const void* base, size_t bytes) {
-  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-  if (!encode) {
+  // thread-safe one-time lookup (calls on different devices run concurrently)
+  static const PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
     cudaDriverEntryPointQueryResult q{};
     void* fn = nullptr;
     CUDA_OK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
     if (!fn || q != cudaDriverEntryPointSuccess)
       throw Failure(FPMM_B200_ECUDA, "cuTensorMapEncodeTiled unavailable");
-    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-  }
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
   CUtensorMap m{};
   constexpr cuuint32_t kRows = rns::kAStage / 128;  // one stage chunk (kBStage == kAStage)
   static_assert(rns::kAStage == rns::kBStage, "A and B stage chunks share the tensor-map box");
@@ -886,7 +908,7 @@ void validate_product(u64 p, int u, int v, u64 lambda, i64 m, i64 k, i64 n, unsi
 }
 
 void product_device(const ProductArgs& a, int device, void* stream, fpmm_b200_timing* tm) {
-  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  DevLock lk(device);
   validate_product(a.p, a.u, a.v, a.lambda, a.m, a.k, a.n, a.flags);
   DeviceCtx& c = ctx(device);
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c.stream;
@@ -945,7 +967,7 @@ struct Prepared {
 
 Prepared* prepare_a_device(const double* dA, i64 lda, i64 m, i64 k, u64 p, int u, int v, unsigned flags,
                            int device, void* stream) {
-  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  DevLock lk(device);
   if (m < 0 || k < 0) throw Failure(FPMM_B200_EERROR, "matrix dimensions must be nonnegative");
   context_check(p, (flags & FPMM_B200_ALLOW_COMPOSITE) != 0);
   if (u < 1 || v < 1) throw Failure(FPMM_B200_EERROR, "multiword product: word counts must be positive");
@@ -973,8 +995,8 @@ Prepared* prepare_a_device(const double* dA, i64 lda, i64 m, i64 k, u64 p, int u
 }
 
 void prepared_free(Prepared* h) {
-  std::lock_guard<std::recursive_mutex> lk(g_mu);
   if (!h) return;
+  DevLock lk(h->device);
   cudaSetDevice(h->device);
   h->words.release();
   delete h;
@@ -982,8 +1004,8 @@ void prepared_free(Prepared* h) {
 
 void product_prepared_device(const Prepared* h, const double* dB, i64 ldb, double* dC, i64 ldc, i64 n, u64 lambda,
                              void* stream, unsigned flags, fpmm_b200_timing* tm) {
-  std::lock_guard<std::recursive_mutex> lk(g_mu);
   if (!h) throw Failure(FPMM_B200_EERROR, "null prepared operand");
+  DevLock lk(h->device);
   const unsigned fl = (flags & ~(FPMM_B200_ENGINE_DMMA | FPMM_B200_ENGINE_I8 | FPMM_B200_ENGINE_RNS)) |
                       (h->engine == kRns  ? FPMM_B200_ENGINE_RNS
                        : h->engine == kI8 ? FPMM_B200_ENGINE_I8
@@ -1059,13 +1081,15 @@ i64 part_rows(i64 m, int parts, int bm) {
 }  // namespace
 
 void product_host(const ProductArgs& a, int ngpus, fpmm_b200_timing* tm) {
-  std::lock_guard<std::recursive_mutex> lk(g_mu);
   validate_product(a.p, a.u, a.v, a.lambda, a.m, a.k, a.n, a.flags);
   if (tm) *tm = fpmm_b200_timing{};
   if (ngpus < 1) throw Failure(FPMM_B200_EERROR, "ngpus must be >= 1");
   const int avail = device_count();
   if (ngpus > avail)
     throw Failure(FPMM_B200_EERROR, "requested " + std::to_string(ngpus) + " GPUs, " + std::to_string(avail) + " visible");
+  std::lock_guard<std::recursive_mutex> all_lk(g_all_mu);
+  std::vector<std::unique_ptr<DevLock>> dev_lks;
+  for (int g = 0; g < ngpus; ++g) dev_lks.push_back(std::make_unique<DevLock>(g));
   if (a.m == 0 || a.n == 0) return;
   if (a.k == 0) {
     for (i64 r = 0; r < a.m; ++r) std::memset(a.C + r * a.ldc, 0, sizeof(double) * a.n);
@@ -1075,7 +1099,12 @@ void product_host(const ProductArgs& a, int ngpus, fpmm_b200_timing* tm) {
                      (a.flags & FPMM_B200_DMMA_EXACT_WORDS) != 0);
   const unsigned chk = a.flags & (FPMM_B200_CHECK_INPUTS | FPMM_B200_CHECK_EXACTNESS);
 
-  if (ngpus == 1) {
+  // FPMM_B200_INPROC_NCCL=1 runs the multi-device branch (communicators from
+  // ncclCommInitAll, B broadcast, per-device C rows) at ngpus = 1 too: the
+  // only way to execute it on a one-GPU box (tests/test_dist_gpu.py)
+  const char* force_env = std::getenv("FPMM_B200_INPROC_NCCL");
+  const bool force_nccl = force_env && std::atoi(force_env) != 0;
+  if (ngpus == 1 && !force_nccl) {
     // Three-stream pipeline over row chunks of A / C: H2D of chunk i+1 and
     // D2H of chunk i-1 overlap the fused kernel on chunk i (PCIe is full
     // duplex); B goes first since every chunk needs its words.
@@ -1147,7 +1176,7 @@ void product_host(const ProductArgs& a, int ngpus, fpmm_b200_timing* tm) {
     return;
   }
 
-  // ngpus > 1: contiguous row blocks of A / C per device; B words packed on
+  // ngpus > 1 (or forced): contiguous row blocks of A / C per device; B words packed on
   // device 0 and broadcast over NCCL (NVLink); each device writes its C rows
   // straight back into the host matrix (row blocks are contiguous).
   g_all.ensure(ngpus);
@@ -1250,7 +1279,7 @@ void product_host(const ProductArgs& a, int ngpus, fpmm_b200_timing* tm) {
 void product_words_host(const double* Aw, i64 a_stride, i64 lda, u64 alpha, int u, const double* Bw,
                         i64 b_stride, i64 ldb, u64 beta, int v, double* C, i64 ldc, i64 m, i64 k,
                         i64 n, u64 p, u64 lambda, unsigned flags, fpmm_b200_timing* tm) {
-  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  DevLock lk(0);
   validate_product(p, u, v, lambda, m, k, n, flags);
   if (m == 0 || n == 0) {
     if (tm) *tm = fpmm_b200_timing{};
@@ -1284,7 +1313,7 @@ void product_words_host(const double* Aw, i64 a_stride, i64 lda, u64 alpha, int 
 
 void decompose_device(const double* dM, i64 ld, i64 rows, i64 cols, u64 p, int u, double* dwords,
                       i64 word_stride, u64* base, int device, void* stream) {
-  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  DevLock lk(device);
   if (u < 1) throw Failure(FPMM_B200_EERROR, "decompose: word count must be positive");
   const u64 alpha = word_base(p, u);
   if (base) *base = alpha;
@@ -1300,7 +1329,7 @@ void decompose_device(const double* dM, i64 ld, i64 rows, i64 cols, u64 p, int u
 
 void decompose_host(const double* M, i64 ld, i64 rows, i64 cols, u64 p, int u, double* words,
                     i64 word_stride, u64* base) {
-  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  DevLock lk(0);
   if (u < 1) throw Failure(FPMM_B200_EERROR, "decompose: word count must be positive");
   DeviceCtx& c = ctx(0);
   const i64 e = rows * cols;
@@ -1320,7 +1349,7 @@ void decompose_host(const double* M, i64 ld, i64 rows, i64 cols, u64 p, int u, d
 
 void accumulate_device(double* dC, i64 ldc, const double* dA, i64 lda, const double* dB, i64 ldb,
                        i64 m, i64 w, i64 n, int device, void* stream) {
-  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  DevLock lk(device);
   if (m < 0 || w < 0 || n < 0) throw Failure(FPMM_B200_EERROR, "accumulate: negative dimensions");
   DeviceCtx& c = ctx(device);
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c.stream;
@@ -1333,7 +1362,7 @@ void accumulate_device(double* dC, i64 ldc, const double* dA, i64 lda, const dou
 
 void accumulate_host(double* C, i64 ldc, const double* A, i64 lda, const double* B, i64 ldb, i64 m,
                      i64 w, i64 n) {
-  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  DevLock lk(0);
   if (m <= 0 || n <= 0 || w <= 0) return;
   DeviceCtx& c = ctx(0);
   cudaStream_t s = c.stream;
@@ -1348,33 +1377,73 @@ void accumulate_host(double* C, i64 ldc, const double* A, i64 lda, const double*
   CUDA_OK(cudaStreamSynchronize(s));
 }
 
-// Alg 2.3 C <- C + A B mod p with C reduced: computed as the (1,1) fused
-// product of A B followed by a modular add of the old C (exact, same value).
+// Alg 2.3 (block_product.hpp:62-73): C <- C + A B mod p, on the device.
+// The reference's panel loop is exact when lambda max(A) max(B) + p - 1 <=
+// 2^t, a contract checked only in FPMM_CONTRACTS builds (check_block_inputs,
+// block_product.hpp:40-54), and its operands need not be residues (e.g. the
+// words of mw_product_words, bounded by alpha).  Here A and B are reduced mod
+// p on the device (exact for integers below 2^53), the exact residue product
+// T runs on the library's engine, and C <- C + T mod p is a device kernel: the
+// reference's value wherever the reference is exact, for any lambda >= 1.
+// CHECK_INPUTS is the contract: entries are non-negative integers below 2^53,
+// C is reduced, and the lambda bound holds on the actual maxima (ContractError).
 void block_gemm_mod_host(double* C, i64 ldc, const double* A, i64 lda, const double* B, i64 ldb,
                          i64 m, i64 k, i64 n, u64 lambda, u64 p, unsigned flags) {
-  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  DevLock lk(0);
   context_check(p, true);
   if (m < 0 || k < 0 || n < 0) throw Failure(FPMM_B200_EERROR, "block_gemm_mod: dimension mismatch");
   if (lambda < 1) throw Failure(FPMM_B200_EINFEASIBLE, "block size infeasible");
-  if (m == 0 || n == 0) return;
-  std::vector<double> T(static_cast<size_t>(m) * n);
-  // words bounded by p-1: the (1,1) product; lambda checked against the bound
-  const u64 lam = std::min<u64>(lambda, static_cast<u64>(std::max<i64>(k, 1)));
-  const u128 peak = static_cast<u128>(lam) * (p - 1) * (p - 1) + (p - 1);
-  if (peak > (u128{1} << kT))
-    throw Failure(FPMM_B200_EINFEASIBLE, "block_gemm_mod: lambda max(A) max(B) + p - 1 exceeds 2^t");
-  ProductArgs pa{A, lda, B, ldb, T.data(), n, m, k, n, p, 1, 1, 1, flags | FPMM_B200_ALLOW_COMPOSITE};
-  product_host(pa, 1, nullptr);
-  for (i64 r = 0; r < m; ++r)
-    for (i64 j = 0; j < n; ++j) {
-      u64 x = static_cast<u64>(C[r * ldc + j]) + static_cast<u64>(T[r * n + j]);
-      C[r * ldc + j] = static_cast<double>(x >= p ? x - p : x);
-    }
+  if (m == 0 || n == 0 || k == 0) return;  // no panel: C unchanged, as the reference's loop
+  DeviceCtx& c = ctx(0);
+  cudaStream_t s = c.stream;
+  double* dA = static_cast<double*>(c.a.get(sizeof(double) * m * k));
+  double* dB = static_cast<double*>(c.b.get(sizeof(double) * k * n));
+  double* dC = static_cast<double*>(c.c.get(sizeof(double) * m * n));
+  double* dT = static_cast<double*>(c.tmp.get(sizeof(double) * m * n));
+  CUDA_OK(cudaMemcpy2DAsync(dA, k * 8, A, lda * 8, k * 8, m, cudaMemcpyHostToDevice, s));
+  CUDA_OK(cudaMemcpy2DAsync(dB, n * 8, B, ldb * 8, n * 8, k, cudaMemcpyHostToDevice, s));
+  CUDA_OK(cudaMemcpy2DAsync(dC, n * 8, C, ldc * 8, n * 8, m, cudaMemcpyHostToDevice, s));
+  if (flags & FPMM_B200_CHECK_INPUTS) {
+    auto* scan = static_cast<unsigned long long*>(c.ver.get(4 * sizeof(unsigned long long)));
+    int* err = reinterpret_cast<int*>(scan + 3);
+    CUDA_OK(cudaMemsetAsync(scan, 0, 4 * sizeof(unsigned long long), s));
+    max_scan_kernel<<<grid_for(m * k, 256), 256, 0, s>>>(dA, k, m, k, scan + 0, err);
+    max_scan_kernel<<<grid_for(k * n, 256), 256, 0, s>>>(dB, n, k, n, scan + 1, err);
+    max_scan_kernel<<<grid_for(m * n, 256), 256, 0, s>>>(dC, n, m, n, scan + 2, err);
+    CUDA_OK(cudaGetLastError());
+    unsigned long long h[4];
+    CUDA_OK(cudaMemcpyAsync(h, scan, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CUDA_OK(cudaStreamSynchronize(s));
+    if (static_cast<int>(h[3] & 0xFFFFFFFFu))
+      throw Failure(FPMM_B200_ECONTRACT, "block_gemm_mod: entries must be non-negative integers below 2^53");
+    if (h[2] >= p) throw Failure(FPMM_B200_ECONTRACT, "block_gemm_mod: C must be reduced mod p");
+    const u64 lam = std::min<u64>(lambda, static_cast<u64>(k));
+    const u128 peak = static_cast<u128>(lam) * h[0] * h[1] + (p - 1);
+    if (peak > (u128{1} << kT))
+      throw Failure(FPMM_B200_ECONTRACT, "block_gemm_mod: lambda max(A) max(B) + p - 1 exceeds 2^t");
+  }
+  const double pf = static_cast<double>(p);
+  reduce_mod_kernel<<<grid_for(m * k, 256), 256, 0, s>>>(dA, k, m, k, pf);
+  reduce_mod_kernel<<<grid_for(k * n, 256), 256, 0, s>>>(dB, n, k, n, pf);
+  reduce_mod_kernel<<<grid_for(m * n, 256), 256, 0, s>>>(dC, n, m, n, pf);
+  CUDA_OK(cudaGetLastError());
+  // T = A B mod p: the (1,1) residue product on the selected (or default) engine
+  const Job j = make_job(m, k, n, p, 1, 1, resolve_engine(flags), (flags & FPMM_B200_DMMA_EXACT_WORDS) != 0);
+  Workspace& ws = c.ws_for(s);
+  void* apack = ws.apack.get(j.apack_bytes);
+  void* bpack = ws.bpack.get(j.bpack_bytes);
+  launch_pack_a(j, dA, k, m, apack, nullptr, s);
+  launch_pack_b(j, dB, n, bpack, nullptr, s);
+  launch_gemm(j, apack, bpack, dT, n, m, s, ws);
+  add_mod_kernel<<<grid_for(m * n, 256), 256, 0, s>>>(dC, n, dT, n, m, n, pf);
+  CUDA_OK(cudaGetLastError());
+  CUDA_OK(cudaMemcpy2DAsync(C, ldc * 8, dC, n * 8, n * 8, m, cudaMemcpyDeviceToHost, s));
+  CUDA_OK(cudaStreamSynchronize(s));
 }
 
 void random_residues_device(double* dM, i64 ld, i64 rows, i64 cols, i64 row0, u64 p, u64 seed, int device,
                             void* stream) {
-  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  DevLock lk(device);
   if (p < 2) throw Failure(FPMM_B200_EERROR, "random_residues: p must exceed 1");
   DeviceCtx& c = ctx(device);
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c.stream;
@@ -1385,8 +1454,53 @@ void random_residues_device(double* dM, i64 ld, i64 rows, i64 cols, i64 row0, u6
   if (!stream) CUDA_OK(cudaStreamSynchronize(s));
 }
 
+// Exact on-device check of C = A B mod p (verify.cuh): range of C, Freivalds
+// trials A (B s) == C s mod p, and sampled exact entries.  counts: [0] entries
+// of C outside [0, p), [1] Freivalds rows that differ (summed over trials),
+// [2] wrong sampled entries, [3..4] (i, j) of the first wrong sample (or -1).
+void verify_device(const double* dA, i64 lda, const double* dB, i64 ldb, const double* dC, i64 ldc, i64 m, i64 k,
+                   i64 n, u64 p, u64 seed, int trials, int samples, int device, void* stream, i64* counts) {
+  DevLock lk(device);
+  if (m < 0 || k < 0 || n < 0) throw Failure(FPMM_B200_EERROR, "verify: dimensions must be nonnegative");
+  if (p < 2 || p >= (u64{1} << 52)) throw Failure(FPMM_B200_EERROR, "verify: modulus must be in [2, 2^52)");
+  if (trials < 0 || samples < 0) throw Failure(FPMM_B200_EERROR, "verify: negative trial / sample count");
+  for (int i = 0; i < 5; ++i) counts[i] = i < 3 ? 0 : -1;
+  if (m == 0 || n == 0) return;
+  DeviceCtx& c = ctx(device);
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c.stream;
+  const size_t words = static_cast<size_t>(n) + static_cast<size_t>(k) + 2 * static_cast<size_t>(m) + 8;
+  u64* base = static_cast<u64*>(c.ver.get(sizeof(u64) * words));
+  unsigned long long* cnt = reinterpret_cast<unsigned long long*>(base);
+  long long* first = reinterpret_cast<long long*>(base + 3);
+  u64* sv = base + 8;
+  u64* yv = sv + n;
+  u64* zv = yv + k;
+  u64* wv = zv + m;
+  CUDA_OK(cudaMemsetAsync(cnt, 0, 3 * sizeof(u64), s));
+  CUDA_OK(cudaMemsetAsync(first, 0xFF, 2 * sizeof(u64), s));
+  verify::range_kernel<<<grid_for(m * n, 256), 256, 0, s>>>(dC, ldc, m, n, p, cnt);
+  const u64 kMax = ~u64{0};
+  auto rows_grid = [](i64 rows) { return grid_for(rows * 32, 256); };
+  for (int t = 0; t < trials; ++t) {
+    const u64 ts = seed * 0x9E3779B97F4A7C15ull + static_cast<u64>(t) * 0xD1B54A32D192ED03ull + 1;
+    verify::rand_vec_kernel<<<grid_for(n, 256), 256, 0, s>>>(sv, n, p, kMax - kMax % p, ts);
+    verify::matvec_mod_kernel<<<rows_grid(k), 256, 0, s>>>(dB, ldb, k, n, sv, p, yv);   // y = B s
+    verify::matvec_mod_kernel<<<rows_grid(m), 256, 0, s>>>(dA, lda, m, k, yv, p, zv);   // z = A y
+    verify::matvec_mod_kernel<<<rows_grid(m), 256, 0, s>>>(dC, ldc, m, n, sv, p, wv);   // w = C s
+    verify::compare_kernel<<<grid_for(m, 256), 256, 0, s>>>(zv, wv, m, cnt);
+  }
+  if (samples > 0)
+    verify::sample_kernel<<<std::max(1, std::min(samples / 8 + 1, 148 * 8)), 256, 0, s>>>(
+        dA, lda, dB, ldb, dC, ldc, m, k, n, p, seed, samples, cnt, first);
+  CUDA_OK(cudaGetLastError());
+  u64 h[5];
+  CUDA_OK(cudaMemcpyAsync(h, base, sizeof(h), cudaMemcpyDeviceToHost, s));
+  CUDA_OK(cudaStreamSynchronize(s));
+  for (int i = 0; i < 5; ++i) counts[i] = static_cast<i64>(h[i]);
+}
+
 double fp64_peak_tflops(int device, int iters) {
-  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  DevLock lk(device);
   DeviceCtx& c = ctx(device);
   int sms = 0;
   CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
@@ -1403,7 +1517,7 @@ double fp64_peak_tflops(int device, int iters) {
 }
 
 double i8_probe_tops(int device, int iters, int mode) {
-  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  DevLock lk(device);
   DeviceCtx& c = ctx(device);
   int sms = 0;
   CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
@@ -1426,7 +1540,7 @@ double i8_probe_tops(int device, int iters, int mode) {
 }
 
 double i8_peak_tops(int device, int iters) {
-  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  DevLock lk(device);
   DeviceCtx& c = ctx(device);
   int sms = 0;
   CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
@@ -1468,7 +1582,8 @@ void nccl_unique_id(void* id) {
 }
 
 void dist_init(const void* id, int nranks, int rank, int device) {
-  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  std::lock_guard<std::recursive_mutex> dlk(g_dist_mu);
+  DevLock lk(device);
   if (nranks < 1 || rank < 0 || rank >= nranks) throw Failure(FPMM_B200_EERROR, "dist_init: bad rank/size");
   if (g_dist.comm) nccl().CommDestroy(g_dist.comm), g_dist.comm = nullptr;
   ctx(device);
@@ -1481,7 +1596,7 @@ void dist_init(const void* id, int nranks, int rank, int device) {
 }
 
 void dist_finalize() {
-  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  std::lock_guard<std::recursive_mutex> dlk(g_dist_mu);
   if (g_dist.comm) nccl().CommDestroy(g_dist.comm);
   g_dist = DistState{};
 }
@@ -1531,20 +1646,59 @@ void dist_product_device(const double* dA_rows, i64 lda, const double* dB, i64 l
                          i64 ldc, double* dC_full, i64 ldc_full, i64 m, i64 k, i64 n, u64 p, int u,
                          int v, u64 lambda, int root, void* stream, unsigned flags,
                          fpmm_b200_timing* tm) {
-  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  std::lock_guard<std::recursive_mutex> dlk(g_dist_mu);
   if (!g_dist.comm) throw Failure(FPMM_B200_EERROR, "dist_mw_product: call fpmm_b200_dist_init first");
-  validate_product(p, u, v, lambda, m, k, n, flags);
-  if (root < 0 || root >= g_dist.nranks) throw Failure(FPMM_B200_EERROR, "dist_mw_product: bad root");
+  DevLock lk(g_dist.device);
   if (tm) *tm = fpmm_b200_timing{};
-  if (m == 0 || n == 0 || k == 0) {
-    if (k == 0 && m > 0 && n > 0) throw Failure(FPMM_B200_EERROR, "dist_mw_product: k == 0 unsupported");
-    return;
-  }
   DeviceCtx& c = ctx(g_dist.device);
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c.stream;
-  const Job j = make_job(m, k, n, p, u, v, resolve_engine(flags), (flags & FPMM_B200_DMMA_EXACT_WORDS) != 0);
+  cudaStream_t so = c.s_out;  // every NCCL call of the partitioner, in one order on every rank
+  const bool is_root = g_dist.rank == root;
+  // Argument checks, agreed on by every rank before any data moves: one
+  // 3-int all-reduce (max) of [status, root gathers, this rank's C rows are
+  // not dense].  A bad argument on any rank -- root's gather target included
+  // -- fails the call on every rank, so no rank is left waiting in a
+  // collective, and every rank gathers iff root passed dC_full (the other
+  // ranks' dC_full is ignored).
+  int code = 0;
+  std::string why;
+  Job j{};
   i64 r0 = 0, rn = 0;
-  dist_rows(m, g_dist.nranks, g_dist.rank, u, v, &r0, &rn);
+  try {
+    validate_product(p, u, v, lambda, m, k, n, flags);
+    if (root < 0 || root >= g_dist.nranks) throw Failure(FPMM_B200_EERROR, "dist_mw_product: bad root");
+    if (k == 0 && m > 0 && n > 0) throw Failure(FPMM_B200_EERROR, "dist_mw_product: k == 0 unsupported");
+    if (m > 0 && n > 0) {
+      j = make_job(m, k, n, p, u, v, resolve_engine(flags), (flags & FPMM_B200_DMMA_EXACT_WORDS) != 0);
+      dist_rows(m, g_dist.nranks, g_dist.rank, u, v, &r0, &rn);
+      if (rn > 0 && (ldc < n || lda < k)) throw Failure(FPMM_B200_EERROR, "dist_mw_product: leading dimension too small");
+      if (is_root && (!dB || ldb < n)) throw Failure(FPMM_B200_EERROR, "dist_mw_product: root needs B (ldb >= n)");
+      if (is_root && dC_full && ldc_full != n)
+        throw Failure(FPMM_B200_EERROR, "dist_mw_product: gather needs a dense target (ldc_full == n)");
+    }
+  } catch (const Failure& e) {
+    code = e.code;
+    why = e.what();
+  }
+  int agree[3] = {code, is_root && dC_full ? 1 : 0, rn > 0 && ldc != n ? 1 : 0};
+  {
+    int* d = static_cast<int*>(c.agree.get(sizeof(agree)));
+    CUDA_OK(cudaMemcpyAsync(d, agree, sizeof(agree), cudaMemcpyHostToDevice, so));
+    NCCL_OK(nccl().AllReduce(d, d, 3, ncclInt32, ncclMax, g_dist.comm, so));
+    CUDA_OK(cudaMemcpyAsync(agree, d, sizeof(agree), cudaMemcpyDeviceToHost, so));
+    CUDA_OK(cudaStreamSynchronize(so));
+  }
+  const bool gather = agree[1] != 0;
+  if (!code && gather && agree[2]) {
+    code = FPMM_B200_EERROR;
+    why = "dist_mw_product: gather needs dense row blocks (ldc == n) on every rank";
+  }
+  if (code) throw Failure(code, why);
+  if (agree[0] || (gather && agree[2]))
+    throw Failure(agree[0] ? agree[0] : FPMM_B200_EERROR,
+                  "dist_mw_product: another rank rejected this call's arguments (status " +
+                      std::to_string(agree[0] ? agree[0] : FPMM_B200_EERROR) + ")");
+  if (m == 0 || n == 0) return;
   Workspace& ws = c.ws_for(s);
   void* apack = ws.apack.get(j.apack_bytes);
   void* bpack = ws.bpack.get(j.bpack_bytes);
@@ -1568,7 +1722,6 @@ void dist_product_device(const double* dA_rows, i64 lda, const double* dB, i64 l
   // Every NCCL call of the partitioner goes to the device's s_out stream, in
   // the same program order on every rank, so products issued on different
   // caller streams never run collectives of the one communicator concurrently.
-  cudaStream_t so = c.s_out;
   if (raw && bchunks > 1) {
     double* dBd = static_cast<double*>(ws.rawb.get(sizeof(double) * k * n));
     if (g_dist.rank == root)
@@ -1613,21 +1766,19 @@ void dist_product_device(const double* dA_rows, i64 lda, const double* dB, i64 l
   // on stream s_out (NCCL P2P) while chunk c+1 computes on s.  Every NCCL call
   // of this product is issued on s_out in the same order on every rank: the
   // broadcast (all of it, or its k-chunks), then one group per chunk index.
-  const auto mine = dC_full ? gather_chunks(j, rn) : std::vector<std::pair<i64, i64>>{{0, rn}};
+  const auto mine = gather ? gather_chunks(j, rn) : std::vector<std::pair<i64, i64>>{{0, rn}};
   int gl = 0;
   for (size_t ci = 0; ci < mine.size(); ++ci) {
     const i64 o = mine[ci].first, l = mine[ci].second;
     if (l <= 0) continue;
     gl += launch_gemm(j, static_cast<uint8_t*>(apack) + static_cast<size_t>(o / j.BM) * j.per_rb_bytes, bpack,
                       dC_rows + o * ldc, ldc, l, s, ws, nullptr, err_ex);
-    if (dC_full) CUDA_OK(cudaEventRecord(c.ev_out[ci], s));
+    if (gather) CUDA_OK(cudaEventRecord(c.ev_out[ci], s));
   }
   CUDA_OK(cudaEventRecord(c.ev[3], s));
   int launches = (rn > 0 ? 1 + gl : 0) + (g_dist.rank == root || raw ? bchunks : 0);
-  if (dC_full) {
+  if (gather) {
     // gather row blocks to root (grouped point-to-point; NCCL has no gather)
-    if (ldc != n || (g_dist.rank == root && ldc_full != n))
-      throw Failure(FPMM_B200_EERROR, "dist_mw_product: gather needs dense row blocks (ld == n)");
     CUDA_OK(cudaStreamWaitEvent(so, c.ev[2], 0));  // root's copies / recvs follow this call's earlier work
     std::vector<std::vector<std::pair<i64, i64>>> theirs(g_dist.nranks);
     std::vector<i64> q0s(g_dist.nranks, 0);
@@ -1680,12 +1831,17 @@ void dist_product_device(const double* dA_rows, i64 lda, const double* dB, i64 l
 }
 
 void finalize_all() {
-  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  std::lock_guard<std::recursive_mutex> dlk(g_dist_mu), alk(g_all_mu);
   if (g_dist.comm) nccl().CommDestroy(g_dist.comm);
   g_dist = DistState{};
   g_all.release();
+  // no call may be in flight on any device (the contexts and their locks go away)
+  std::lock_guard<std::mutex> tl(g_ctx_mu);
   for (auto& c : g_ctx)
-    if (c) c->release();
+    if (c) {
+      std::lock_guard<std::recursive_mutex> l(c->mu);
+      c->release();
+    }
   g_ctx.clear();
 }
 

@@ -57,6 +57,8 @@ void block_gemm_mod_host(double* C, i64 ldc, const double* A, i64 lda, const dou
 unsigned select_engine(i64 m, i64 k, i64 n, u64 p);
 
 int device_count();
+void verify_device(const double* dA, i64 lda, const double* dB, i64 ldb, const double* dC, i64 ldc, i64 m, i64 k,
+                   i64 n, u64 p, u64 seed, int trials, int samples, int device, void* stream, i64* counts);
 void random_residues_device(double* dM, i64 ld, i64 rows, i64 cols, i64 row0, u64 p, u64 seed, int device,
                             void* stream);
 double fp64_peak_tflops(int device, int iters);

@@ -437,6 +437,46 @@ __global__ void __launch_bounds__(128) accumulate_kernel(double* __restrict__ C,
 
 namespace fpmm_b200 {
 
+// block_gemm_mod helpers (block_product.hpp:62-73 on the device).
+// M <- M mod p in place: exact (fmod of a non-negative integer below 2^53).
+__global__ void reduce_mod_kernel(double* __restrict__ M, i64 ld, i64 rows, i64 cols, double p) {
+  for (i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; e < rows * cols;
+       e += static_cast<i64>(gridDim.x) * blockDim.x) {
+    double* x = M + (e / cols) * ld + e % cols;
+    *x = fmod(*x, p);
+  }
+}
+
+// C <- (C + T) mod p for residues C, T < p (< 2^52: the sum is exact)
+__global__ void add_mod_kernel(double* __restrict__ Cm, i64 ldc, const double* __restrict__ T, i64 ldt, i64 rows,
+                               i64 cols, double p) {
+  for (i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; e < rows * cols;
+       e += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 r = e / cols, c = e % cols;
+    const double x = Cm[r * ldc + c] + T[r * ldt + c];
+    Cm[r * ldc + c] = x >= p ? x - p : x;
+  }
+}
+
+// the contract's operand scan: max entry (atomicMax) and whether every entry
+// is a non-negative integer below 2^53 (err bit 1 otherwise)
+__global__ void max_scan_kernel(const double* __restrict__ M, i64 ld, i64 rows, i64 cols,
+                                unsigned long long* maxv, int* err) {
+  unsigned long long mx = 0;
+  for (i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; e < rows * cols;
+       e += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const double v = M[(e / cols) * ld + e % cols];
+    if (!(v >= 0.0 && v < 9007199254740992.0 && v == floor(v))) {
+      atomicOr(err, 1);
+      continue;
+    }
+    mx = max(mx, static_cast<unsigned long long>(v));
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) mx = max(mx, __shfl_down_sync(0xffffffffu, mx, off));
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(maxv, mx);
+}
+
 // Device-side synthetic residues for large benchmarks: element e of a
 // rows x cols slice starting at global row row0 (global index g = (row0+i)*cols + j) is the first draw r = splitmix64(seed ^ (g * 2^8 + t)),
 // t = 0, 1, ..., below reject_at (the largest multiple of p), reduced mod p:

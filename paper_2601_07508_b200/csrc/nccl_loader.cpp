@@ -36,6 +36,7 @@ const NcclApi& nccl() {
       bind(h, api.CommInitAll, "ncclCommInitAll");
       bind(h, api.CommDestroy, "ncclCommDestroy");
       bind(h, api.Broadcast, "ncclBroadcast");
+      bind(h, api.AllReduce, "ncclAllReduce");
       bind(h, api.Send, "ncclSend");
       bind(h, api.Recv, "ncclRecv");
       bind(h, api.GroupStart, "ncclGroupStart");

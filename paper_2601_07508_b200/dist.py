@@ -86,7 +86,7 @@ def mw_product_device(A_rows, B, C_rows, p: int, u: int, v: int, lambda_: int, m
     n = C_rows.shape[1]
     bptr, ldb = (B.data_ptr(), _dev_ld(B)) if B is not None else (None, max(n, 1))
     cf, ldcf = (C_full.data_ptr(), _dev_ld(C_full)) if C_full is not None else (None, max(n, 1))
-    sp = _stream_handle(stream)
+    sp = _stream_handle(stream, A_rows.device.index)
     _check(lib().fpmm_b200_dist_mw_product_device(
         A_rows.data_ptr(), max(k, 1) if A_rows.shape[0] <= 1 else _dev_ld(A_rows), bptr, ldb,
         C_rows.data_ptr(), max(n, 1) if C_rows.shape[0] <= 1 else _dev_ld(C_rows), cf, ldcf, m, k, n,
@@ -125,8 +125,10 @@ def mw_product_host(A_rows_host, B_host, C_host, p: int, u: int, v: int, lambda_
         raise Error("non-root ranks must know n (pass scratch={'n': n})")
     dC = buf("Crows", (a.shape[0], n))
     dCf = buf("Cfull", (m, n)) if C_host is not None else None
+    # the product runs on the stream that carries the H2D copies above (torch's
+    # current stream), so the packers never read A or B before they land
     mw_product_device(dA, dB, dC, p, u, v, lambda_, m, root=root, C_full=dCf, timing=timing,
-                      flags=flags)
+                      flags=flags, stream=torch.cuda.current_stream())
     if C_host is not None:
         torch.as_tensor(C_host).copy_(dCf)
     torch.cuda.synchronize()

@@ -216,6 +216,51 @@ def test_block_gemm_mod():
     assert (C == want).all()
 
 
+@pytest.mark.parametrize("bits", [40, 47, 52])
+def test_block_gemm_mod_word_operands(bits):
+    """Reference semantics above 2^26.5: word-sized operands (the way
+    mw_product_words calls it, max = alpha) with the reference's lambda for
+    that bound; equal to the oracle's restatement of the panel loop and to the
+    exact value.  Operands >= p (below the contract bound) reduce first."""
+    p = F.prev_prime(1 << bits)
+    alpha = F.word_base(p, 2)
+    rng = np.random.default_rng(bits)
+    m, k, n = 37, 300, 29
+    A = rng.integers(0, alpha + 1, size=(m, k)).astype(np.float64)
+    B = rng.integers(0, alpha + 1, size=(k, n)).astype(np.float64)
+    C0 = rng.integers(0, p, size=(m, n)).astype(np.float64)
+    lam = F.max_block_size(alpha, alpha, p)
+    assert lam is not None and lam >= 1
+    Fc = F.FpContext.make(p)
+    C = C0.copy()
+    F.block_gemm_mod(C, A, B, lam, Fc, flags=F.CHECK_INPUTS)
+    Co = C0.copy()
+    assert O.lib().fo_block_gemm_mod(O._ptr(Co), O._ptr(A), k, O._ptr(B), n, m, k, n, lam, p) == 0
+    want = (C0.astype(np.int64).astype(object) + A.astype(np.int64).astype(object).dot(
+        B.astype(np.int64).astype(object))) % p
+    assert (C == Co).all() and (C.astype(np.int64).astype(object) == want).all()
+    # entries >= p: a small bound keeps the contract; every engine agrees
+    A2 = A.copy()
+    A2[0, :] = float(p + 5)
+    B2 = rng.integers(0, 3, size=(k, n)).astype(np.float64)
+    want2 = (C0.astype(np.int64).astype(object) + A2.astype(np.int64).astype(object).dot(
+        B2.astype(np.int64).astype(object))) % p
+    for eng in (F.ENGINE_RNS, F.ENGINE_I8, F.ENGINE_DMMA):
+        C2 = C0.copy()
+        F.block_gemm_mod(C2, A2, B2, 1, Fc, flags=eng)
+        assert (C2.astype(np.int64).astype(object) == want2).all()
+    # the contract: lambda beyond the bound (when the bound is below k), unreduced C
+    if lam < k:
+        with pytest.raises(F.ContractError):
+            F.block_gemm_mod(C0.copy(), A, B, k, Fc, flags=F.CHECK_INPUTS)
+    Cbad = C0.copy()
+    Cbad[0, 0] = float(p)
+    with pytest.raises(F.ContractError):
+        F.block_gemm_mod(Cbad, A, B, lam, Fc, flags=F.CHECK_INPUTS)
+    with pytest.raises(F.InfeasibleError):
+        F.block_gemm_mod(C0.copy(), A, B, 0, Fc)
+
+
 def test_check_inputs_flag():
     p = F.prev_prime(1 << 30)
     A = np.full((4, 4), float(p))  # not reduced
@@ -237,6 +282,7 @@ def test_device_tensors_and_streams():
     assert (dC.cpu().numpy() == want).all()
     s = torch.cuda.Stream()
     dC2 = torch.zeros_like(dC)
+    s.wait_stream(torch.cuda.current_stream())  # the zeroing above runs on torch's stream
     F.mw_product_device(dA, dB, dC2, p, 2, 2, 1, stream=s)
     assert (dC2.cpu().numpy() == want).all()
     # strided device views
@@ -376,6 +422,7 @@ def test_cuda_graph_capture(engine):
     C = torch.empty((m, n), dtype=torch.float64, device="cuda")
     F.random_residues_device(A, p, 3)
     F.random_residues_device(B, p, 4)
+    torch.cuda.synchronize()  # generated on torch's current stream; the product runs on s
     fl = F.ASYNC  # the fixture's default engine is added by the library binding
     s = torch.cuda.Stream()
     with torch.cuda.stream(s):

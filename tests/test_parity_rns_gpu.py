@@ -98,6 +98,7 @@ def test_rns_strided_device_and_split():
     dB = torch.from_numpy(B).cuda()[:, :n]
     dC = torch.zeros((m, n + 7), dtype=torch.float64, device="cuda")[:, :n]
     s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())  # dC's zeroing runs on torch's stream
     pl = F.plan_for_modulus(p, m, k, n)
     F.mw_product_device(dA, dB, dC, p, pl.u, pl.v, pl.lambda_, stream=s, flags=RNS)
     s.synchronize()
