@@ -254,6 +254,20 @@ int fpmm_b200_dist_mw_product_device(const double* dA_rows, int64_t lda, const d
  * when stream is NULL. */
 int fpmm_b200_random_residues_device(double* dM, int64_t ld, int64_t rows, int64_t cols, int64_t row0,
                                      uint64_t p, uint64_t seed, int device, void* stream);
+/* Exact on-device check of a device-resident product C = A B mod p, for sizes
+ * a CPU recomputation cannot reach (the analogue of the reference's
+ * oracle-equivalence check, driver.cpp:37-140 / first_mismatch at
+ * oracle.hpp:71-81).  All arithmetic is exact (128-bit dot products):
+ *   counts[0] = entries of C that are not integers in [0, p)
+ *   counts[1] = rows with A (B s) != C s (mod p), summed over `trials`
+ *               Freivalds trials with uniform s in [0, p)^n (a wrong C passes
+ *               one trial with probability <= 1/p)
+ *   counts[2] = wrong entries among `samples` sampled (i, j) (corners first)
+ *   counts[3], counts[4] = (i, j) of the first wrong sample, or -1
+ * Synchronous on `stream` (NULL = the library's stream for `device`). */
+int fpmm_b200_verify_device(const double* dA, int64_t lda, const double* dB, int64_t ldb, const double* dC,
+                            int64_t ldc, int64_t m, int64_t k, int64_t n, uint64_t p, uint64_t seed, int trials,
+                            int samples, int device, void* stream, int64_t* counts);
 /* Measured FP64 tensor-pipe peak (TFLOP/s): a DMMA.8x8x4-only loop. */
 int fpmm_b200_fp64_peak(int device, int iters, double* tflops);
 /* Measured int8 tensor-core peak (TOP/s): back-to-back tcgen05.mma.kind::i8

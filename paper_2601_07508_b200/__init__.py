@@ -29,7 +29,7 @@ __all__ = [
     "decompose", "mw_product", "mw_product_words", "mw_product_workspace",
     "mw_product_workspace_words", "mw_product_concat", "mw_product_concat_words",
     "block_gemm_mod", "GemmKernel", "kernel_by_name", "b200_kernel", "mw_product_device",
-    "decompose_device", "accumulate_device", "device_count", "finalize", "lib", "LIB_PATH",
+    "decompose_device", "accumulate_device", "verify_device", "device_count", "finalize", "lib", "LIB_PATH",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -169,6 +169,8 @@ def lib():
                                                    u64, i32, i32, u64, i32, vp, C.c_uint,
                                                    C.POINTER(Timing)]),
         "fpmm_b200_random_residues_device": (i32, [vp, i64, i64, i64, i64, u64, u64, i32, vp]),
+        "fpmm_b200_verify_device": (i32, [vp, i64, vp, i64, vp, i64, i64, i64, i64, u64, u64, i32, i32,
+                                          i32, vp, _i64p]),
         "fpmm_b200_fp64_peak": (i32, [i32, i32, C.POINTER(C.c_double)]),
         "fpmm_b200_i8_peak": (i32, [i32, i32, C.POINTER(C.c_double)]),
         "fpmm_b200_prepare_a_device": (i32, [vp, i64, i64, i64, u64, i32, i32, C.c_uint, i32, vp,
@@ -659,6 +661,25 @@ def random_residues_device(M, p: int, seed: int, row0: int = 0, stream=None) -> 
     sp = _stream_handle(stream, M.device.index)
     _check(lib().fpmm_b200_random_residues_device(M.data_ptr(), _dev_ld(M), rows, cols, row0, p,
                                                   seed, M.device.index, sp))
+
+
+def verify_device(A, B, Cm, p: int, *, seed: int = 1, trials: int = 2, samples: int = 64,
+                  stream=None) -> dict:
+    """Exact on-device check of C = A B mod p (device tensors): C's range,
+    Freivalds trials A (B s) == C s mod p, sampled exact entries
+    (fpmm_b200_verify_device).  ``ok`` is True when every count is zero."""
+    m, k = A.shape
+    n = B.shape[1]
+    if B.shape[0] != k or tuple(Cm.shape) != (m, n):
+        raise Error("verify: dimension mismatch")
+    out = (C.c_int64 * 5)()
+    _check(lib().fpmm_b200_verify_device(A.data_ptr(), _dev_ld(A), B.data_ptr(), _dev_ld(B), Cm.data_ptr(),
+                                         _dev_ld(Cm), m, k, n, p, seed, trials, samples, A.device.index,
+                                         _stream_handle(stream, A.device.index), out))
+    r = {"range": out[0], "freivalds_rows": out[1], "samples_bad": out[2], "first_bad": (out[3], out[4]),
+         "trials": trials, "samples": samples}
+    r["ok"] = out[0] == 0 and out[1] == 0 and out[2] == 0
+    return r
 
 
 def i8_peak(device: int = 0, iters: int = 200000) -> float:

@@ -284,6 +284,15 @@ int fpmm_b200_random_residues_device(double* dM, int64_t ld, int64_t rows, int64
   return guarded([&] { random_residues_device(dM, ld, rows, cols, row0, p, seed, device, stream); });
 }
 
+int fpmm_b200_verify_device(const double* dA, int64_t lda, const double* dB, int64_t ldb, const double* dC,
+                            int64_t ldc, int64_t m, int64_t k, int64_t n, uint64_t p, uint64_t seed, int trials,
+                            int samples, int device, void* stream, int64_t* counts) {
+  return guarded([&] {
+    if (!counts) throw Failure(FPMM_B200_EERROR, "verify: counts must not be NULL");
+    verify_device(dA, lda, dB, ldb, dC, ldc, m, k, n, p, seed, trials, samples, device, stream, counts);
+  });
+}
+
 int fpmm_b200_fp64_peak(int device, int iters, double* tflops) {
   return guarded([&] { *tflops = fp64_peak_tflops(device, iters); });
 }

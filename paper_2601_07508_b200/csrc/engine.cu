@@ -706,6 +706,28 @@ CUtensorMap chunk_map(const void* base, size_t bytes) {
   return m;
 }
 
+// RNS split-K: split when the output has too few pair tiles for the SM
+// pairs, and one slice per exact int32 segment for long K (split-major: each
+// wave streams one K-chunk of its panels); n_mod is planned for the full K.
+int rns_splits(const Job& j, i64 rows) {
+  const i64 tiles0 = ((rows + rns::kPairM - 1) / rns::kPairM) * j.NB;
+  int splits = 1;
+  if (tiles0 > 0 && tiles0 < 74) {
+    const i64 want = (74 + tiles0 - 1) / tiles0;
+    splits = pick_splits(tiles0, 74, std::min<i64>(want, j.KB / 16), std::min<i64>(j.KB / 16, 32));
+  }
+  if (j.KB > j.rp.seg_kb) splits = std::max<int>(splits, (j.KB + j.rp.seg_kb - 1) / j.rp.seg_kb);
+  const int per = (j.KB + splits - 1) / splits;
+  return (j.KB + per - 1) / per;
+}
+
+// the fused CRT (no separate reconstruction kernel) applies without split-K;
+// FPMM_B200_RNS_FUSED=0 keeps the separate rns_crt_kernel (A/B and tests)
+bool rns_fused(const Job& j, i64 rows) {
+  const char* e = std::getenv("FPMM_B200_RNS_FUSED");
+  return !(e && std::atoi(e) == 0) && rns_splits(j, rows) == 1;
+}
+
 int launch_gemm_rns_rows(const Job& j, const void* apack, const void* bpack, double* C, i64 ldc, i64 rows,
                          cudaStream_t s, cudaEvent_t mid, Workspace& ws) {
   rns::Params q = j.rp;
@@ -717,20 +739,13 @@ int launch_gemm_rns_rows(const Job& j, const void* apack, const void* bpack, dou
   q.ldc = ldc;
   q.m = rows;
   q.MB = static_cast<int>((rows + rns::kPairM - 1) / rns::kPairM);
-  // split-K when the output has too few pair tiles for the SM pairs, and one
-  // slice per exact int32 segment for long K (split-major: each wave streams
-  // one K-chunk of its panels); the slices' residues are summed mod m_i by
-  // the CRT kernel, which covers the full K (n_mod is planned for it)
-  const i64 tiles0 = static_cast<i64>(q.MB) * q.NB;
-  int splits = 1;
-  if (tiles0 > 0 && tiles0 < 74) {
-    const i64 want = (74 + tiles0 - 1) / tiles0;
-    splits = pick_splits(tiles0, 74, std::min<i64>(want, j.KB / 16), std::min<i64>(j.KB / 16, 32));
-  }
-  if (j.KB > q.seg_kb) splits = std::max<int>(splits, (j.KB + q.seg_kb - 1) / q.seg_kb);
+  const int splits = rns_splits(j, rows);
   q.kb_per_split = (j.KB + splits - 1) / splits;
-  splits = (j.KB + q.kb_per_split - 1) / q.kb_per_split;
   q.splits = splits;
+  // splits == 1: the CRT runs in the epilogue of each tile's last modulus
+  // pass (tile-major passes, residues parked per CTA); otherwise the slices'
+  // residues are summed mod m_i by rns_crt_kernel after the kernel
+  q.fused = rns_fused(j, rows) ? 1 : 0;
   int dev = 0;
   CUDA_OK(cudaGetDevice(&dev));
   int sms = 148;
@@ -760,8 +775,10 @@ int launch_gemm_rns_rows(const Job& j, const void* apack, const void* bpack, dou
     max_pairs[dev & 63] = std::min(clusters, sms / 2);
   }
   const unsigned grid = 2 * static_cast<unsigned>(std::max<i64>(1, std::min<i64>(items, max_pairs[dev & 63])));
-  // residue bytes of every item: n bytes per output element and slice
-  q.scratch = static_cast<uint8_t*>(ws.scratch.get(static_cast<size_t>(items) * 2 * j.nmod * rns::kSlotPerMod));
+  // residue bytes: fused, one block per CTA (reused tile after tile: ~71 MB at
+  // n = 15, L2-resident); else every item's, n bytes per output element and slice
+  const size_t slots = q.fused ? static_cast<size_t>(grid) : static_cast<size_t>(items) * 2;
+  q.scratch = static_cast<uint8_t*>(ws.scratch.get(slots * j.nmod * rns::kSlotPerMod));
   q.group = rns::kGroup;
   if (const char* d = std::getenv("FPMM_B200_RNS_GROUP")) q.group = std::max(1, std::atoi(d));
   static bool configured[64] = {};
@@ -769,10 +786,7 @@ int launch_gemm_rns_rows(const Job& j, const void* apack, const void* bpack, dou
     CUDA_OK(cudaFuncSetAttribute(rns::rns_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, rns::kSmem));
     configured[dev & 63] = true;
   }
-  rns::rns_kernel<<<grid, rns::kThreads, rns::kSmem, s>>>(q);
-  CUDA_OK(cudaGetLastError());
-  if (mid) CUDA_OK(cudaEventRecord(mid, s));
-  // CRT of every tile (slices summed mod m_i first) straight into C
+  // the CRT constants and C: for rns_crt_kernel, or the fused epilogue
   rns::CrtParams cp = j.rcp;
   cp.R = q.scratch;
   cp.C = C;
@@ -780,8 +794,15 @@ int launch_gemm_rns_rows(const Job& j, const void* apack, const void* bpack, dou
   cp.m = rows;
   cp.n = j.n;
   cp.MB = q.MB, cp.NB = q.NB, cp.splits = splits, cp.group = q.group;
-  const i64 tiles = static_cast<i64>(q.MB) * q.NB;
   const int wpl = std::max(1, (bitsize(j.p - 1) + 7) / 8);
+  q.crt = cp;
+  q.wpl = wpl;
+  rns::rns_kernel<<<grid, rns::kThreads, rns::kSmem, s>>>(q);
+  CUDA_OK(cudaGetLastError());
+  if (mid) CUDA_OK(cudaEventRecord(mid, s));
+  if (q.fused) return 1;
+  // CRT of every tile (slices summed mod m_i first) straight into C
+  const i64 tiles = static_cast<i64>(q.MB) * q.NB;
   switch (wpl) {
     case 1: rns::rns_crt_kernel<1><<<static_cast<unsigned>(2 * tiles), 256, 0, s>>>(cp); break;
     case 2: rns::rns_crt_kernel<2><<<static_cast<unsigned>(2 * tiles), 256, 0, s>>>(cp); break;
@@ -807,7 +828,8 @@ int launch_gemm_rns(const Job& j, const void* apack, const void* bpack, double* 
   size_t budget = kRnsResidueBudget;
   if (const char* e = std::getenv("FPMM_B200_RNS_RESIDUE_BUDGET")) budget = std::strtoull(e, nullptr, 10);
   const i64 chunk = std::max<i64>(1, static_cast<i64>(budget / per_pair_row));
-  if (pair_rows <= chunk) return launch_gemm_rns_rows(j, apack, bpack, C, ldc, rows, s, mid, ws);
+  // (the fused CRT parks one residue block per CTA, whatever the size)
+  if (pair_rows <= chunk || rns_fused(j, rows)) return launch_gemm_rns_rows(j, apack, bpack, C, ldc, rows, s, mid, ws);
   int launches = 0;
   for (i64 pr = 0; pr < pair_rows; pr += chunk) {
     const i64 r0 = pr * rns::kPairM, rn = std::min<i64>(rows - r0, chunk * rns::kPairM);

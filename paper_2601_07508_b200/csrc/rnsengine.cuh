@@ -73,6 +73,34 @@ constexpr int kSmem = kStages * kStageBytes + 1024;
 constexpr int kSlotPerMod = kBM * kNT;  // scratch bytes per modulus per CTA tile (32 KB)
 constexpr int kGroup = 16;              // pair-tile rows per rasterisation group
 
+// ------------------------------------------------------------------ CRT
+// C = X mod p from the parked residue bytes of every tile (summed over the
+// split-K slices mod m_i first: residues are additive):
+//   X mod p = (sum r_i W_i - t (M mod p)) mod p,  t = round(sum r_i y_i / m_i),
+// W_i = y_i M_i mod p (7 bytes), g_i = round(2^19 y_i / m_i) (3 bytes).  Both
+// sums are evaluated byte-plane by byte-plane with dp4a over groups of four
+// moduli: the residue words of four moduli are transposed (PRMT) so one word
+// holds one element's four residues, and plane b accumulates
+// sum_i r_i byte_b(W_i) (< 20 * 255^2 < 2^21).  That is 10 dp4a per element
+// per four moduli.  The fixed-point error of t is <= n 255 2^-20 <= 0.005,
+// inside the plan's range margin (|X| / M <= 1/2.03).
+constexpr int kCrtPlanes = 10;                 // 7 byte planes of W, 3 of g
+constexpr int kCrtGroups = (kMaxMod + 3) / 4;  // groups of four moduli
+struct CrtParams {
+  const uint8_t* R;  // residue blocks, as parked by rns_kernel
+  double* C;
+  i64 ldc, m, n;
+  int MB, NB, nmod, splits, group;
+  unsigned long long p, mu, two32, two32_sh, Mp, Mp_sh;
+  // n <= 16 finalisation (S < 16 * 255 * p): q = umulhi(S >> s_shift, inv32)
+  // is floor(S/p) - {0,1,2}; t (M mod p) by a 32-bit Shoup product
+  int s_shift;     // max(0, bits(p) - 20): S >> s_shift < 2^32 and 2^s_shift < p
+  uint32_t inv32;  // floor(2^(s_shift + 32) / p)
+  uint32_t Mp_sh32;  // floor((M mod p) 2^32 / p)
+  uint32_t mod[kMaxMod];
+  uint32_t wb[kCrtGroups][kCrtPlanes];  // byte b of W_i (b < 7) / g_i (b >= 7) for the group's 4 moduli
+};
+
 // Per-modulus constants (host: rns_plan in rules.cpp).
 struct Params {
   // 2-D byte views (128-byte rows) of the packed operands for the pair TMA
@@ -91,6 +119,7 @@ struct Params {
   int group;         // pair-tile rows per rasterisation group
   int small_t;       // seg_kb * kBK * 255^2 < 2^24: products reduce without the 16-bit split
   int flat;          // PassIter order (see there)
+  int fused;         // CRT in the last modulus pass of each tile (see rns_kernel); needs splits == 1
   unsigned epi_sleep_ns;  // epilogue's accumulator wait: sleep between polls (ns), 0 = suspending try_wait
   i64 split_stride;
   unsigned long long p, mu;            // Barrett: mu = floor(2^64 / p)
@@ -102,6 +131,8 @@ struct Params {
   uint32_t magic[kMaxMod];  // ceil(2^32 / m): floor(s/m) = umulhi(s, magic) for s < 2^32 / m
   uint32_t g[kMaxMod];      // round(2^24 y_i / m_i)
   uint32_t w_lo[kMaxMod], w_hi[kMaxMod];  // W_i = y_i M_i mod p
+  CrtParams crt;  // fused: the reconstruction constants and C (crt.R unused)
+  int wpl;        // fused: byte planes of W_i (ceil(bits(p - 1) / 8))
 };
 
 struct PackParams {
@@ -375,7 +406,7 @@ __device__ __forceinline__ uint4* scratch_at(uint8_t* slot, int i, int half, int
 // k = 256 outer-product shape), so mod_small applies to it directly.
 template <bool SMALL>
 __device__ __forceinline__ void park32(const uint32_t (&v)[32], uint32_t m, uint32_t negm, uint32_t c16, uint32_t magic,
-                                       bool acc, uint4* dst0, uint4* dst1) {
+                                       bool acc, uint4* dst0, uint4* dst1, bool stream = true) {
   uint32_t w[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
@@ -403,41 +434,20 @@ __device__ __forceinline__ void park32(const uint32_t (&v)[32], uint32_t m, uint
       w[q] = word;
     }
   }
-  // streaming stores: read back only by the CRT kernel
-  __stcs(dst0, make_uint4(w[0], w[1], w[2], w[3]));
-  __stcs(dst1, make_uint4(w[4], w[5], w[6], w[7]));
+  if (stream) {  // streaming stores: read back only by the CRT kernel
+    __stcs(dst0, make_uint4(w[0], w[1], w[2], w[3]));
+    __stcs(dst1, make_uint4(w[4], w[5], w[6], w[7]));
+  } else {  // fused: read back by this thread n - 1 passes later, kept in L2
+    *dst0 = make_uint4(w[0], w[1], w[2], w[3]);
+    *dst1 = make_uint4(w[4], w[5], w[6], w[7]);
+  }
 }
 
-// ------------------------------------------------------------------ CRT
-// C = X mod p from the parked residue bytes of every tile (summed over the
-// split-K slices mod m_i first: residues are additive):
-//   X mod p = (sum r_i W_i - t (M mod p)) mod p,  t = round(sum r_i y_i / m_i),
-// W_i = y_i M_i mod p (7 bytes), g_i = round(2^19 y_i / m_i) (3 bytes).  Both
-// sums are evaluated byte-plane by byte-plane with dp4a over groups of four
-// moduli: the residue words of four moduli are transposed (PRMT) so one word
-// holds one element's four residues, and plane b accumulates
-// sum_i r_i byte_b(W_i) (< 20 * 255^2 < 2^21).  That is 10 dp4a per element
-// per four moduli.  The fixed-point error of t is <= n 255 2^-20 <= 0.005,
-// inside the plan's range margin (|X| / M <= 1/2.03).
-constexpr int kCrtPlanes = 10;                 // 7 byte planes of W, 3 of g
-constexpr int kCrtGroups = (kMaxMod + 3) / 4;  // groups of four moduli
-struct CrtParams {
-  const uint8_t* R;  // residue blocks, as parked by rns_kernel
-  double* C;
-  i64 ldc, m, n;
-  int MB, NB, nmod, splits, group;
-  unsigned long long p, mu, two32, two32_sh, Mp, Mp_sh;
-  // n <= 16 finalisation (S < 16 * 255 * p): q = umulhi(S >> s_shift, inv32)
-  // is floor(S/p) - {0,1,2}; t (M mod p) by a 32-bit Shoup product
-  int s_shift;     // max(0, bits(p) - 20): S >> s_shift < 2^32 and 2^s_shift < p
-  uint32_t inv32;  // floor(2^(s_shift + 32) / p)
-  uint32_t Mp_sh32;  // floor((M mod p) 2^32 / p)
-  uint32_t mod[kMaxMod];
-  uint32_t wb[kCrtGroups][kCrtPlanes];  // byte b of W_i (b < 7) / g_i (b >= 7) for the group's 4 moduli
-};
-
 // The n residue words of 4-column step c (SPLIT: the slices' residues summed mod m_i).
-template <bool SPLIT>
+// NC: the read-only (non-coherent) load path, for residues parked by an
+// earlier kernel; the fused epilogue reads bytes it wrote itself in the same
+// kernel and uses plain loads.
+template <bool SPLIT, bool NC = true>
 __device__ __forceinline__ void crt_load(const CrtParams& P, const uint8_t* __restrict__ pthr, i64 slice_stride, int c,
                                          uint32_t (&rw)[kMaxMod]) {
   const uint8_t* pc = pthr + (c >> 2) * (16 * kBM) + (c & 3) * 4;
@@ -446,7 +456,8 @@ __device__ __forceinline__ void crt_load(const CrtParams& P, const uint8_t* __re
     if (i >= P.nmod) {
       rw[i] = 0;
     } else if (!SPLIT) {
-      rw[i] = __ldg(reinterpret_cast<const uint32_t*>(pc + i * kSlotPerMod));
+      rw[i] = NC ? __ldg(reinterpret_cast<const uint32_t*>(pc + i * kSlotPerMod))
+                 : *reinterpret_cast<const uint32_t*>(pc + i * kSlotPerMod);
     } else {
       uint32_t r = *reinterpret_cast<const uint32_t*>(pc + i * kSlotPerMod);
       for (int s = 1; s < P.splits; ++s) {  // add the other slices' residues mod m_i
@@ -556,16 +567,31 @@ __device__ __forceinline__ void crt_step(const CrtParams& P, int c, i64 colh, do
 // CRT of one thread's 128 columns, four per step; all n residue words of a
 // step are loaded before any is used.  (Pipelining the next step's loads
 // measured 15-20% slower: the extra registers cost a resident block per SM.)
-template <int WPL, bool SPLIT>
+template <int WPL, bool SPLIT, bool NC = true>
 __device__ __forceinline__ void crt_row(const CrtParams& P, const uint8_t* __restrict__ pthr, i64 slice_stride,
-                                        i64 colh, double* __restrict__ dst_row) {
-  constexpr int kSteps = (kNT / 2) / 4;
+                                        i64 colh, double* __restrict__ dst_row, int c_begin = 0,
+                                        int c_end = (kNT / 2) / 4) {
 #pragma unroll 1
-  for (int c = 0; c < kSteps; ++c) {
+  for (int c = c_begin; c < c_end; ++c) {
     if (colh + c * 4 >= P.n) break;
     uint32_t rw[kMaxMod];
-    crt_load<SPLIT>(P, pthr, slice_stride, c, rw);
+    crt_load<SPLIT, NC>(P, pthr, slice_stride, c, rw);
     crt_step<WPL>(P, c, colh, dst_row, rw);
+  }
+}
+
+// The fused epilogue's CRT: 4-column steps [c_begin, c_end) of one row half,
+// from residues this thread parked itself (runtime byte-plane count).
+__device__ __forceinline__ void crt_row_fused(const CrtParams& P, int wpl, const uint8_t* pthr, i64 colh,
+                                              double* dst_row, int c_begin, int c_end) {
+  switch (wpl) {
+    case 1: return crt_row<1, false, false>(P, pthr, 0, colh, dst_row, c_begin, c_end);
+    case 2: return crt_row<2, false, false>(P, pthr, 0, colh, dst_row, c_begin, c_end);
+    case 3: return crt_row<3, false, false>(P, pthr, 0, colh, dst_row, c_begin, c_end);
+    case 4: return crt_row<4, false, false>(P, pthr, 0, colh, dst_row, c_begin, c_end);
+    case 5: return crt_row<5, false, false>(P, pthr, 0, colh, dst_row, c_begin, c_end);
+    case 6: return crt_row<6, false, false>(P, pthr, 0, colh, dst_row, c_begin, c_end);
+    default: return crt_row<7, false, false>(P, pthr, 0, colh, dst_row, c_begin, c_end);
   }
 }
 
@@ -659,8 +685,10 @@ __device__ __forceinline__ void commit_pair(uint64_t* bar) {
       : "memory");
 }
 
-// The pair's work items (modulus i, item t) in order.  flat: one sequence
-// over i * total + t, so every pair runs the same number of items (+-1) and
+// The pair's work items (modulus i, item t) in order.  fused: tile-major,
+// the n moduli of tile t back to back (t = pair, pair + npairs, ...), so the
+// last pass of a tile can rebuild C from residues the pair parked itself.
+// flat: one sequence over i * total + t, so every pair runs the same number of items (+-1) and
 // the pairs that share a wave's panels stay in lockstep across moduli;
 // otherwise each modulus restarts at t = pair (pairs with one item fewer per
 // modulus run ahead into the next modulus).
@@ -668,7 +696,9 @@ struct PassIter {
   int i, t;
   __device__ __forceinline__ PassIter(int pair) : i(0), t(pair) {}
   __device__ __forceinline__ void next(const Params& P, int pair, int npairs, int total) {
-    if (P.flat) {
+    if (P.fused) {  // every modulus of a tile back to back, then the pair's next tile
+      if (++i == P.nmod) i = 0, t += npairs;
+    } else if (P.flat) {
       const int g = i * total + t + npairs;
       i = g / total;
       t = g - i * total;
@@ -678,6 +708,8 @@ struct PassIter {
     }
   }
   __device__ __forceinline__ bool valid(const Params& P, int total) const { return i < P.nmod && t < total; }
+  // fused order: the last modulus of the tile (its epilogue runs the CRT)
+  __device__ __forceinline__ bool last(const Params& P) const { return P.fused && i == P.nmod - 1; }
 };
 
 // The pair (cluster of 2 CTAs on neighbouring SMs) computes a 256 x 256 tile:
@@ -789,10 +821,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
     }
   } else {
     // ---------------- epilogue: warps 2..9 of both CTAs ----------------
-    // Pass (modulus i, tile t): T_i mod m_i is parked in the tile's residue
-    // block in HBM; the pass of the last modulus then reads the tile's n
-    // residue bytes per element back and runs the CRT into C.  Each thread
-    // only ever reads bytes it wrote itself.
+    // Pass (modulus i, tile t): T_i mod m_i is parked in a residue block.
+    // fused (splits == 1): the block is the CTA's own, the passes of a tile
+    // run back to back, and the epilogue of its last modulus reads the n
+    // residue bytes per element back (each thread only reads bytes it wrote
+    // itself) and runs the CRT into C.  Otherwise every tile has its block in
+    // HBM and rns_crt_kernel rebuilds C after the kernel.
     const int quad = warp % 4;
     const int col0 = ((warp - 2) / 4) * kEpiCols;  // this warp's first accumulator column
     const int half = col0 / (kNT / 2);
@@ -808,7 +842,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
         const int kb0 = it.ks * P.kb_per_split;
         const int nkb = max(0, min(P.KB, kb0 + P.kb_per_split) - kb0);
         const int nseg = max(1, (nkb + P.seg_kb - 1) / P.seg_kb);
-        uint8_t* slot = P.scratch + (static_cast<i64>(t) * 2 + rank) * P.nmod * kSlotPerMod;
+        // fused: one residue block per CTA, reused tile after tile (L2-resident)
+        uint8_t* slot = P.scratch + ((P.fused ? static_cast<i64>(pair) : static_cast<i64>(t)) * 2 + rank) * P.nmod *
+                                        kSlotPerMod;
         for (int seg = 0; seg < nseg; ++seg, ++pass) {
           const int b = pass & 1;
           if (P.epi_sleep_ns) dev::mbar_wait_sleep(&tmem_full[b], (pass >> 1) & 1, P.epi_sleep_ns);
@@ -827,8 +863,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
             }
             uint4* d0 = scratch_at(slot, i, half, c0 / 16, row_in_tile);
             uint4* d1 = scratch_at(slot, i, half, c0 / 16 + 1, row_in_tile);
-            if (P.small_t) park32<true>(v, m, nm, c16, mg, seg > 0, d0, d1);
-            else park32<false>(v, m, nm, c16, mg, seg > 0, d0, d1);
+            if (P.small_t) park32<true>(v, m, nm, c16, mg, seg > 0, d0, d1, !P.fused);
+            else park32<false>(v, m, nm, c16, mg, seg > 0, d0, d1, !P.fused);
+          }
+        }
+        if (pi.last(P)) {
+          // every modulus of this tile is parked (by this very thread, for its
+          // row and columns): rebuild C = X mod p by the CRT while the MMAs of
+          // the pair's next tile run on the other accumulator
+          const i64 row = (2 * static_cast<i64>(it.tm) + rank) * kBM + row_in_tile;
+          if (row < P.crt.m) {
+            const int cb = (col0 % (kNT / 2)) / 4;  // first 4-column step of this warp in its half
+            const i64 colh = static_cast<i64>(it.tn) * kNT + half * (kNT / 2);
+            const uint8_t* pthr = slot + (static_cast<i64>(half) * 8 * kBM + row_in_tile) * 16;
+            crt_row_fused(P.crt, P.wpl, pthr, colh, P.crt.C + row * P.crt.ldc + colh, cb, cb + kEpiCols / 4);
           }
         }
       }

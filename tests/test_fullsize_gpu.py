@@ -124,8 +124,9 @@ def test_c3_32768_cubed_52bit():
 
 
 def test_c3_row_blocks_forced(monkeypatch):
-    """C3's shape class with the RNS residue budget forced small (many row
-    blocks, ragged last block) equals the single-block product bitwise."""
+    """C3's shape class through the separate-CRT path (FPMM_B200_RNS_FUSED=0)
+    with the residue budget forced small (many row blocks, ragged last block)
+    equals the fused product bitwise."""
     import torch
     m, k, n = 8192 + 300, 32768, 4096
     p, A, B = _inputs(m, k, n, 52)
@@ -133,10 +134,30 @@ def test_c3_row_blocks_forced(monkeypatch):
     C1 = torch.empty((m, n), dtype=torch.float64, device="cuda")
     C2 = torch.empty((m, n), dtype=torch.float64, device="cuda")
     F.mw_product_device(A, B, C1, p, pl.u, pl.v, pl.lambda_, flags=F.ENGINE_RNS)
+    monkeypatch.setenv("FPMM_B200_RNS_FUSED", "0")
     monkeypatch.setenv("FPMM_B200_RNS_RESIDUE_BUDGET", str(300 << 20))
     F.mw_product_device(A, B, C2, p, pl.u, pl.v, pl.lambda_, flags=F.ENGINE_RNS)
     assert torch.equal(C1, C2)
     _check(A, B, C2, p)
+
+
+@pytest.mark.parametrize("shape,bits", [((8192, 8192, 8192), 20), ((8192, 8192, 8192), 52), ((1000, 3000, 777), 45),
+                                        ((65536, 256, 4096), 40), ((300, 100000, 5000), 33), ((5000, 64, 300), 26)])
+def test_rns_fused_crt_equals_separate(monkeypatch, shape, bits):
+    """The CRT in the last modulus pass's epilogue (tile-major passes,
+    residues parked per CTA) gives the separate rns_crt_kernel's C bitwise,
+    on full and ragged tiles and a split-K shape (which keeps the separate CRT)."""
+    import torch
+    m, k, n = shape
+    p, A, B = _inputs(m, k, n, bits)
+    pl = F.plan_for_modulus(p, m, k, n)
+    C1 = torch.empty((m, n), dtype=torch.float64, device="cuda")
+    C2 = torch.full((m, n), -1.0, dtype=torch.float64, device="cuda")
+    F.mw_product_device(A, B, C1, p, pl.u, pl.v, pl.lambda_, flags=F.ENGINE_RNS)
+    monkeypatch.setenv("FPMM_B200_RNS_FUSED", "0")
+    F.mw_product_device(A, B, C2, p, pl.u, pl.v, pl.lambda_, flags=F.ENGINE_RNS)
+    assert torch.equal(C1, C2)
+    assert F.verify_device(A, B, C1, p)["ok"]
 
 
 def test_c4_tall_reduction_48bit():
