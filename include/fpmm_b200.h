@@ -50,7 +50,8 @@ typedef enum {
  *   DMMA: the paper's FP64 multiword product on the FP64 tensor pipe (mma.sync .f64)
  *   I8  : base-256 multiword words on tcgen05.mma.kind::i8 (int32 TMEM accumulators)
  *   RNS : byte residues modulo pairwise-coprime m_i <= 256, one kind::i8 GEMM per
- *         modulus, CRT reconstruction mod p fused into the epilogue
+ *         modulus (epilogue parks T_i mod m_i, one byte per element), then one
+ *         CRT reconstruction kernel mod p
  * no flag = the library default: I8 or RNS, whichever a B200 time model
  * predicts faster for (m, k, n, p) (I8 for prepared A, where n is unknown) */
 #define FPMM_B200_ENGINE_DMMA 0x10u
@@ -88,7 +89,7 @@ typedef struct {
 typedef struct {
   double h2d_ms;       /* host -> device copies (host-buffer entry points)   */
   double pack_ms;      /* decomposition kernels (A and B words)              */
-  double gemm_ms;      /* fused multiword GEMM + reconstruction epilogue     */
+  double gemm_ms;      /* product kernel(s): GEMM, epilogue and (RNS) CRT     */
   double comm_ms;      /* NCCL broadcast / gather                            */
   double d2h_ms;       /* device -> host copy of C                           */
   double total_ms;     /* whole call                                         */

@@ -721,11 +721,16 @@ int rns_splits(const Job& j, i64 rows) {
   return (j.KB + per - 1) / per;
 }
 
-// the fused CRT (no separate reconstruction kernel) applies without split-K;
-// FPMM_B200_RNS_FUSED=0 keeps the separate rns_crt_kernel (A/B and tests)
+// The CRT in the epilogue of each tile's last modulus pass (tile-major
+// passes, no separate reconstruction kernel): opt-in with FPMM_B200_RNS_FUSED=1,
+// without split-K only.  Measured slower than rns_crt_kernel on every config
+// (8192^3 sweep -9%, C3 -32%, C5 -37%: profiles/round2/ab_fused.txt): the
+// epilogue's 8 warps per CTA run the CRT at a fraction of a full-occupancy
+// kernel's issue rate, and the per-CTA residue blocks (71 MB at n = 15) do
+// not stay in L2 next to the operand panels, so no HBM traffic is saved.
 bool rns_fused(const Job& j, i64 rows) {
   const char* e = std::getenv("FPMM_B200_RNS_FUSED");
-  return !(e && std::atoi(e) == 0) && rns_splits(j, rows) == 1;
+  return e && std::atoi(e) != 0 && rns_splits(j, rows) == 1;
 }
 
 int launch_gemm_rns_rows(const Job& j, const void* apack, const void* bpack, double* C, i64 ldc, i64 rows,

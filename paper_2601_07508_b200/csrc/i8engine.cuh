@@ -6,14 +6,16 @@
 // and each T_s is an exact integer sum of digit products (<= 255^2 each)
 // computed by tcgen05.mma.kind::i8 into int32 TMEM accumulators.  Read as
 // unsigned, a T_s block is exact while pairs(s) * Kseg * 255^2 < 2^32, so K is
-// processed in segments of at most Kseg; the epilogue folds the 2D-1 blocks
-// with Horner's rule mod p (Barrett) and accumulates the segments.
+// processed in segments of at most Kseg; the epilogue reduces every block mod p
+// and forms sum_s (256^s mod p) T_s with independent Shoup products (no Horner
+// chain), accumulating the segments.
 //
-// One CTA computes a 128 x 32 tile of C.  B's digits are concatenated along
-// N (B_cat = [B_0 | .. | B_{D-1}], N_mma = 32 D) and the MMA of A digit i is
-// issued at TMEM column offset 32 i, so digit pair (i, j) lands in column
-// block i + j = s: one MMA per A digit per k-step builds every T_s at once,
-// in (2D-1) * 32 <= 416 TMEM columns.
+// One CTA computes a 128 x NT tile of C, NT = 256/128/64/64/32/32/32 for
+// D = 1..7 (the widest with (2D-1) NT <= 512 TMEM columns and D NT <= 256).
+// B's digits are concatenated along N (B_cat = [B_0 | .. | B_{D-1}],
+// N_mma = D NT) and the MMA of A digit i is issued at TMEM column offset
+// NT i, so digit pair (i, j) lands in column block i + j = s: one MMA per A
+// digit per k-step builds every T_s at once.
 //
 // Warp roles: warp 0 TMA producer (1-D bulk copies of pre-packed chunks),
 // warp 1 TMEM allocator + single-thread MMA issuer, warps 2-5 epilogue

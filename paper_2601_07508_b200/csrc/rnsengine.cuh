@@ -822,7 +822,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
   } else {
     // ---------------- epilogue: warps 2..9 of both CTAs ----------------
     // Pass (modulus i, tile t): T_i mod m_i is parked in a residue block.
-    // fused (splits == 1): the block is the CTA's own, the passes of a tile
+    // fused (opt-in, splits == 1): the block is the CTA's own, the passes of a tile
     // run back to back, and the epilogue of its last modulus reads the n
     // residue bytes per element back (each thread only reads bytes it wrote
     // itself) and runs the CRT into C.  Otherwise every tile has its block in

@@ -133,6 +133,7 @@ def test_c3_row_blocks_forced(monkeypatch):
     pl = F.plan_for_modulus(p, m, k, n)
     C1 = torch.empty((m, n), dtype=torch.float64, device="cuda")
     C2 = torch.empty((m, n), dtype=torch.float64, device="cuda")
+    monkeypatch.setenv("FPMM_B200_RNS_FUSED", "1")
     F.mw_product_device(A, B, C1, p, pl.u, pl.v, pl.lambda_, flags=F.ENGINE_RNS)
     monkeypatch.setenv("FPMM_B200_RNS_FUSED", "0")
     monkeypatch.setenv("FPMM_B200_RNS_RESIDUE_BUDGET", str(300 << 20))
@@ -153,6 +154,7 @@ def test_rns_fused_crt_equals_separate(monkeypatch, shape, bits):
     pl = F.plan_for_modulus(p, m, k, n)
     C1 = torch.empty((m, n), dtype=torch.float64, device="cuda")
     C2 = torch.full((m, n), -1.0, dtype=torch.float64, device="cuda")
+    monkeypatch.setenv("FPMM_B200_RNS_FUSED", "1")
     F.mw_product_device(A, B, C1, p, pl.u, pl.v, pl.lambda_, flags=F.ENGINE_RNS)
     monkeypatch.setenv("FPMM_B200_RNS_FUSED", "0")
     F.mw_product_device(A, B, C2, p, pl.u, pl.v, pl.lambda_, flags=F.ENGINE_RNS)
