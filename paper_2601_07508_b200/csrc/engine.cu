@@ -751,6 +751,10 @@ int launch_gemm_rns_rows(const Job& j, const void* apack, const void* bpack, dou
   // pass (tile-major passes, residues parked per CTA); otherwise the slices'
   // residues are summed mod m_i by rns_crt_kernel after the kernel
   q.fused = rns_fused(j, rows) ? 1 : 0;
+  // two epilogue groups on alternate passes (one K segment per pass); off: FPMM_B200_RNS_PINGPONG=0
+  q.pingpong = (!q.fused && q.kb_per_split <= q.seg_kb) ? 1 : 0;
+  if (const char* e = std::getenv("FPMM_B200_RNS_PINGPONG")) q.pingpong = q.pingpong && std::atoi(e) != 0;
+  if (const char* e = std::getenv("FPMM_B200_RNS_DEBUG")) q.debug = std::atoi(e);
   int dev = 0;
   CUDA_OK(cudaGetDevice(&dev));
   int sms = 148;
@@ -808,6 +812,25 @@ int launch_gemm_rns_rows(const Job& j, const void* apack, const void* bpack, dou
   if (q.fused) return 1;
   // CRT of every tile (slices summed mod m_i first) straight into C
   const i64 tiles = static_cast<i64>(q.MB) * q.NB;
+  // one K slice: the kernel specialised on the plane and group counts
+  // (FPMM_B200_RNS_CRT_SPEC=0 keeps the generic one, for A/B)
+  static const bool spec = [] {
+    const char* e = std::getenv("FPMM_B200_RNS_CRT_SPEC");
+    return !(e && std::atoi(e) == 0);
+  }();
+  if (splits == 1 && spec) {
+    using K = void (*)(rns::CrtParams);
+#define FPMM_CRT_ROW(W) \
+  {rns::rns_crt_spec_kernel<W, 1>, rns::rns_crt_spec_kernel<W, 2>, rns::rns_crt_spec_kernel<W, 3>, \
+   rns::rns_crt_spec_kernel<W, 4>, rns::rns_crt_spec_kernel<W, 5>}
+    static const K table[7][5] = {FPMM_CRT_ROW(1), FPMM_CRT_ROW(2), FPMM_CRT_ROW(3), FPMM_CRT_ROW(4),
+                                  FPMM_CRT_ROW(5), FPMM_CRT_ROW(6), FPMM_CRT_ROW(7)};
+#undef FPMM_CRT_ROW
+    const int ng = (j.nmod + 3) / 4;
+    table[std::min(wpl, 7) - 1][ng - 1]<<<static_cast<unsigned>(2 * tiles), 256, 0, s>>>(cp);
+    CUDA_OK(cudaGetLastError());
+    return 2;
+  }
   switch (wpl) {
     case 1: rns::rns_crt_kernel<1><<<static_cast<unsigned>(2 * tiles), 256, 0, s>>>(cp); break;
     case 2: rns::rns_crt_kernel<2><<<static_cast<unsigned>(2 * tiles), 256, 0, s>>>(cp); break;

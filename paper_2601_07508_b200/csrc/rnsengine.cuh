@@ -62,12 +62,17 @@ constexpr int kBStage = kBH * kBK;   // this CTA's 128 columns of B (16 KB)
 constexpr int kStageBytes = kAStage + kBStage;
 constexpr int kStages = 12 * 64 / kBK;  // 192 KB of stages (kBK 64, 128, 192, 256)
 #ifndef FPMM_B200_RNS_EPI_WARPS
-#define FPMM_B200_RNS_EPI_WARPS 8
+#define FPMM_B200_RNS_EPI_WARPS 16
 #endif
 constexpr int kEpiWarps = FPMM_B200_RNS_EPI_WARPS;  // 8 or 16: 4 TMEM lane quadrants x column groups
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kEpiCols = 4 * kNT / kEpiWarps;        // accumulator columns per epilogue warp
 static_assert(kEpiWarps == 8 || kEpiWarps == 16, "epilogue warps");
+// epilogue: drain all of a warp's accumulator columns, release, then reduce
+// (1) or release after the last 32-column load (0)
+#ifndef FPMM_B200_RNS_DRAIN_FIRST
+#define FPMM_B200_RNS_DRAIN_FIRST 1
+#endif
 static_assert(kBK % 64 == 0 && kBK <= 256, "stage k-depth: 64, 128 or 256 bytes");
 constexpr int kSmem = kStages * kStageBytes + 1024;
 constexpr int kSlotPerMod = kBM * kNT;  // scratch bytes per modulus per CTA tile (32 KB)
@@ -120,6 +125,9 @@ struct Params {
   int small_t;       // seg_kb * kBK * 255^2 < 2^24: products reduce without the 16-bit split
   int flat;          // PassIter order (see there)
   int fused;         // CRT in the last modulus pass of each tile (see rns_kernel); needs splits == 1
+  int debug;         // timing experiments only (wrong C): 1 no residue stores, 2 no reduction or stores, 4 no MMAs
+  int pingpong;      // 16 epilogue warps as two groups of 8 taking alternate passes (kEpiWarps == 16;
+                     // one K segment per pass, not fused)
   unsigned epi_sleep_ns;  // epilogue's accumulator wait: sleep between polls (ns), 0 = suspending try_wait
   i64 split_stride;
   unsigned long long p, mu;            // Barrett: mu = floor(2^64 / p)
@@ -595,6 +603,151 @@ __device__ __forceinline__ void crt_row_fused(const CrtParams& P, int wpl, const
   }
 }
 
+// ---- CRT specialised on the plane and group counts (splits == 1) ----
+// The generic crt_step above spends ~156 instructions per element at n = 15
+// (ncu source page, profiles/round2): runtime modulus / plane checks, the
+// accumulators zeroed before the first dp4a, constants fetched with LDC, one
+// 4-byte load per modulus and 4 columns.  With WPL (byte planes of W_i) and
+// NG (groups of four moduli) compile-time, every dp4a takes its weight word
+// straight from the constant bank, the first group initialises the planes,
+// and each modulus' 16-byte chunk of a row is loaded once (CW columns per
+// load) for CW / 4 steps.
+
+// 4 columns -> 4 outputs mod p from the n residue words of the columns
+// (rw[i]: modulus i, bytes = columns).  Same arithmetic as crt_step.
+template <int WPL, int NG>
+__device__ __forceinline__ void crt4_spec(const CrtParams& P, const uint32_t (&rw)[4 * NG], double (&out)[4]) {
+  constexpr int NP = WPL + 3;  // planes: W bytes 0..WPL-1, then g bytes 0..2
+  uint32_t acc[4][NP];
+#pragma unroll
+  for (int gi = 0; gi < NG; ++gi) {
+    const uint32_t a0 = rw[4 * gi], a1 = rw[4 * gi + 1], a2 = rw[4 * gi + 2], a3 = rw[4 * gi + 3];
+    const uint32_t u0 = __byte_perm(a0, a1, 0x5140), u1 = __byte_perm(a0, a1, 0x7362);
+    const uint32_t u2 = __byte_perm(a2, a3, 0x5140), u3 = __byte_perm(a2, a3, 0x7362);
+    const uint32_t t[4] = {__byte_perm(u0, u2, 0x5410), __byte_perm(u0, u2, 0x7632), __byte_perm(u1, u3, 0x5410),
+                           __byte_perm(u1, u3, 0x7632)};
+#pragma unroll
+    for (int pb = 0; pb < NP; ++pb) {
+      const uint32_t wb = P.wb[gi][pb < WPL ? pb : 7 + (pb - WPL)];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[e][pb] = __dp4a(t[e], wb, gi == 0 ? 0u : acc[e][pb]);
+    }
+  }
+  const unsigned long long p = P.p;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const uint32_t* a = acc[e];
+    const uint32_t g0 = a[WPL], g1 = a[WPL + 1], g2 = a[WPL + 2];
+    // t = round(F / 2^19), F = g0 + 2^8 g1 + 2^16 g2 (see crt_step)
+    const uint32_t tt = (g1 + (g2 << 8) + (g0 >> 8) + 1024u) >> 11;
+    unsigned long long sm, tmod;
+    if (NG <= 4) {  // n <= 16: S = sum_i r_i W_i <= 16 * 255 * (p - 1) < 2^64
+      unsigned long long S = a[0];
+#pragma unroll
+      for (int b = 1; b < (WPL < 4 ? WPL : 4); ++b) S = mad_wide(a[b], 1u << (8 * b), S);
+      if (WPL > 4) {
+        uint32_t hi = a[4];
+#pragma unroll
+        for (int b = 5; b < WPL; ++b) hi += a[b] << (8 * (b - 4));
+        S += static_cast<unsigned long long>(hi) << 32;
+      }
+      const uint32_t q = __umulhi(static_cast<uint32_t>(S >> P.s_shift), P.inv32);
+      unsigned long long r = S - mad_wide(q, static_cast<uint32_t>(p), 0ull) -
+                             (static_cast<unsigned long long>(q * static_cast<uint32_t>(p >> 32)) << 32);
+      r = r >= p ? r - p : r;
+      sm = r >= p ? r - p : r;
+      const uint32_t qt = __umulhi(tt, P.Mp_sh32);
+      const unsigned long long tm = mad_wide(tt, static_cast<uint32_t>(P.Mp), 0ull) +
+                                    (static_cast<unsigned long long>(tt * static_cast<uint32_t>(P.Mp >> 32)) << 32) -
+                                    mad_wide(qt, static_cast<uint32_t>(p), 0ull) -
+                                    (static_cast<unsigned long long>(qt * static_cast<uint32_t>(p >> 32)) << 32);
+      tmod = tm >= p ? tm - p : tm;
+    } else {
+      unsigned long long lo = a[0];
+#pragma unroll
+      for (int b = 1; b < (WPL < 4 ? WPL : 4); ++b) lo += static_cast<unsigned long long>(a[b]) << (8 * b);
+      unsigned long long hi = 0;
+#pragma unroll
+      for (int b = 4; b < WPL; ++b) hi += static_cast<unsigned long long>(a[b]) << (8 * (b - 4));
+      sm = barrett(dev::shoup_mulmod(hi, P.two32, P.two32_sh, p) + lo, p, P.mu);
+      tmod = dev::shoup_mulmod(tt, P.Mp, P.Mp_sh, p);
+    }
+    const unsigned long long r = sm >= tmod ? sm - tmod : sm + p - tmod;
+    out[e] = __longlong_as_double(static_cast<long long>(r | 0x4330000000000000ull)) - 4503599627370496.0;
+  }
+}
+
+#ifndef FPMM_B200_CRT_CW
+#define FPMM_B200_CRT_CW 8
+#endif
+constexpr int kCrtCW = FPMM_B200_CRT_CW;  // columns per residue load (4, 8 or 16 bytes)
+static_assert(kCrtCW == 4 || kCrtCW == 8 || kCrtCW == 16, "CRT load width");
+
+template <int CW>
+struct CrtWord;
+template <>
+struct CrtWord<4> {
+  using T = uint32_t;
+  static __device__ __forceinline__ void split(T v, uint32_t (&w)[1]) { w[0] = v; }
+};
+template <>
+struct CrtWord<8> {
+  using T = uint2;
+  static __device__ __forceinline__ void split(T v, uint32_t (&w)[2]) { w[0] = v.x, w[1] = v.y; }
+};
+template <>
+struct CrtWord<16> {
+  using T = uint4;
+  static __device__ __forceinline__ void split(T v, uint32_t (&w)[4]) { w[0] = v.x, w[1] = v.y, w[2] = v.z, w[3] = v.w; }
+};
+
+// One CTA per (tile, CTA half of the pair), one thread per row half: the
+// 128 columns of its row half in 16-column chunks ([i][half][c16][row][16 B]).
+template <int WPL, int NG>
+__global__ void __launch_bounds__(256) rns_crt_spec_kernel(const __grid_constant__ CrtParams P) {
+  using W = CrtWord<kCrtCW>;
+  const int tile = blockIdx.x >> 1, rank = blockIdx.x & 1;
+  const int row_in_tile = threadIdx.x % kBM, half = threadIdx.x / kBM;
+  Params q{};
+  q.MB = P.MB, q.NB = P.NB, q.splits = 1, q.group = P.group;
+  const Item it = item_of(tile, q);
+  const i64 row = (2 * static_cast<i64>(it.tm) + rank) * kBM + row_in_tile;
+  if (row >= P.m) return;
+  const i64 colh = static_cast<i64>(it.tn) * kNT + half * (kNT / 2);
+  const uint8_t* pthr = P.R + (static_cast<i64>(tile) * 2 + rank) * P.nmod * kSlotPerMod +
+                        (static_cast<i64>(half) * 8 * kBM + row_in_tile) * 16;
+  double* dst_row = P.C + row * P.ldc + colh;
+#pragma unroll 1
+  for (int cl = 0; cl < kNT / 2; cl += kCrtCW) {
+    if (colh + cl >= P.n) break;
+    const uint8_t* pc = pthr + (cl / 16) * (16 * kBM) + (cl % 16);
+    uint32_t w[4 * NG][kCrtCW / 4];
+#pragma unroll
+    for (int i = 0; i < 4 * NG; ++i) {
+      typename W::T v{};
+      if (i < 4 * (NG - 1) || i < P.nmod) v = __ldg(reinterpret_cast<const typename W::T*>(pc + i * kSlotPerMod));
+      W::split(v, w[i]);
+    }
+#pragma unroll
+    for (int s = 0; s < kCrtCW / 4; ++s) {
+      const i64 col0 = colh + cl + 4 * s;
+      if (col0 >= P.n) break;
+      uint32_t rw[4 * NG];
+#pragma unroll
+      for (int i = 0; i < 4 * NG; ++i) rw[i] = w[i][s];
+      double out[4];
+      crt4_spec<WPL, NG>(P, rw, out);
+      double* dst = dst_row + cl + 4 * s;
+      if (col0 + 4 <= P.n && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+        *reinterpret_cast<double2*>(dst) = make_double2(out[0], out[1]);
+        *reinterpret_cast<double2*>(dst + 2) = make_double2(out[2], out[3]);
+      } else {
+        for (int e = 0; e < 4 && col0 + e < P.n; ++e) dst[e] = out[e];
+      }
+    }
+  }
+}
+
 // WPL = byte planes of W_i (ceil(bits(p - 1) / 8)): the kernel skips the zero planes.
 template <int WPL>
 __global__ void __launch_bounds__(256) rns_crt_kernel(const __grid_constant__ CrtParams P) {
@@ -740,7 +893,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
     }
     for (int b = 0; b < 2; ++b) {
       dev::mbar_init(&tmem_full[b], 1);
-      dev::mbar_init(&tmem_empty[b], 2 * kEpiWarps);
+      dev::mbar_init(&tmem_empty[b], 2 * (P.pingpong ? kEpiWarps / 2 : kEpiWarps));
     }
     dev::fence_barrier_init();
   }
@@ -810,7 +963,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
               for (int tk = 0; tk < kKSteps; ++tk) {
                 const uint64_t ad = i8::smem_desc(a0 + tk * 2 * (kBM / 8) * 128, (kBM / 8) * 128, 128);
                 const uint64_t bd = i8::smem_desc(b0 + tk * 2 * (kBH / 8) * 128, (kBH / 8) * 128, 128);
-                mma_i8_pair(tacc, ad, bd, idesc, (kb > kstart || tk > 0) ? 1u : 0u);
+                if (!(P.debug & 4)) mma_i8_pair(tacc, ad, bd, idesc, (kb > kstart || tk > 0) ? 1u : 0u);
               }
               commit_pair(&empty[s]);  // frees stage s in both CTAs
             }
@@ -827,8 +980,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
     // residue bytes per element back (each thread only reads bytes it wrote
     // itself) and runs the CRT into C.  Otherwise every tile has its block in
     // HBM and rns_crt_kernel rebuilds C after the kernel.
+    // pingpong: warps 2..9 take the even passes (accumulator 0), 10..17 the
+    // odd ones, each warp 128 columns; a group reduces and stores one pass
+    // while the other drains the next, so short-K passes (k = 256: about as
+    // long as their epilogue) no longer serialise MMA and epilogue.
+    const bool pp = kEpiWarps == 16 && P.pingpong;
+    const int ew = warp - 2;
+    const int group = pp ? ew / 8 : 0;
+    const int wcols = pp ? 128 : kEpiCols;  // accumulator columns of this warp
     const int quad = warp % 4;
-    const int col0 = ((warp - 2) / 4) * kEpiCols;  // this warp's first accumulator column
+    const int col0 = pp ? ((ew % 8) / 4) * 128 : (ew / 4) * kEpiCols;  // this warp's first accumulator column
     const int half = col0 / (kNT / 2);
     const int row_in_tile = quad * 32 + lane;
     const uint32_t tlane = static_cast<uint32_t>(quad * 32) << 16;
@@ -847,22 +1008,55 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
                                         kSlotPerMod;
         for (int seg = 0; seg < nseg; ++seg, ++pass) {
           const int b = pass & 1;
+          if (pp && b != group) continue;  // the other group's pass
           if (P.epi_sleep_ns) dev::mbar_wait_sleep(&tmem_full[b], (pass >> 1) & 1, P.epi_sleep_ns);
           else dev::mbar_wait(&tmem_full[b], (pass >> 1) & 1);
           i8::fence_after();
           const uint32_t tcol = tbase + tlane + b * kNT + half * (kNT / 2);
+#if FPMM_B200_RNS_DRAIN_FIRST
+          if (!pp) {
+            // drain every column of this warp into registers first, then hand
+            // the accumulator back and reduce: the MMAs of pass + 2 no longer
+            // wait for the reduction and stores (short-K passes, e.g. the
+            // k = 256 outer product, are as short as the epilogue itself)
+            const int cb = col0 % (kNT / 2);
+            uint32_t v[kEpiCols / 32][32];
+#pragma unroll
+            for (int q = 0; q < kEpiCols / 32; ++q) i8::tmem_ld32(tcol + cb + 32 * q, v[q]);
+            i8::tmem_wait_ld();
+            i8::fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(leader_tmem_empty + b * 8);
+#pragma unroll
+            for (int q = 0; q < kEpiCols / 32; ++q) {
+              const int c0 = cb + 32 * q;
+              uint4* d0 = scratch_at(slot, i, half, c0 / 16, row_in_tile);
+              uint4* d1 = scratch_at(slot, i, half, c0 / 16 + 1, row_in_tile);
+              if (P.small_t) park32<true>(v[q], m, nm, c16, mg, seg > 0, d0, d1, !P.fused);
+              else park32<false>(v[q], m, nm, c16, mg, seg > 0, d0, d1, !P.fused);
+            }
+          } else
+#endif
 #pragma unroll 1
-          for (int c0 = col0 % (kNT / 2); c0 < col0 % (kNT / 2) + kEpiCols; c0 += 32) {
+          for (int c0 = col0 % (kNT / 2); c0 < col0 % (kNT / 2) + wcols; c0 += 32) {
             uint32_t v[32];
             i8::tmem_ld32(tcol + c0, v);
             i8::tmem_wait_ld();
-            if (c0 + 32 == col0 % (kNT / 2) + kEpiCols) {  // all of this warp's columns are in registers: release
+            if (c0 + 32 == col0 % (kNT / 2) + wcols) {  // all of this warp's columns are in registers: release
               i8::fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive_cluster(leader_tmem_empty + b * 8);
             }
+            if (P.debug & 2) continue;
             uint4* d0 = scratch_at(slot, i, half, c0 / 16, row_in_tile);
             uint4* d1 = scratch_at(slot, i, half, c0 / 16 + 1, row_in_tile);
+            if (P.debug & 1) {  // reduction without the stores (the result kept live)
+              uint32_t x = 0;
+#pragma unroll
+              for (int e = 0; e < 32; ++e) x += mod_small(v[e], nm, mg);
+              if (x == 0xFFFFFFFFu) *d0 = make_uint4(x, x, x, x);
+              continue;
+            }
             if (P.small_t) park32<true>(v, m, nm, c16, mg, seg > 0, d0, d1, !P.fused);
             else park32<false>(v, m, nm, c16, mg, seg > 0, d0, d1, !P.fused);
           }
@@ -876,7 +1070,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
             const int cb = (col0 % (kNT / 2)) / 4;  // first 4-column step of this warp in its half
             const i64 colh = static_cast<i64>(it.tn) * kNT + half * (kNT / 2);
             const uint8_t* pthr = slot + (static_cast<i64>(half) * 8 * kBM + row_in_tile) * 16;
-            crt_row_fused(P.crt, P.wpl, pthr, colh, P.crt.C + row * P.crt.ldc + colh, cb, cb + kEpiCols / 4);
+            crt_row_fused(P.crt, P.wpl, pthr, colh, P.crt.C + row * P.crt.ldc + colh, cb, cb + wcols / 4);
           }
         }
       }
