@@ -368,6 +368,45 @@ Job make_i8_job(i64 m, i64 k, i64 n, u64 p) {
   return j;
 }
 
+// The one-reduction CRT finalisation (rns_crt_spec_kernel): with r_i the
+// residues of X, S = sum_i r_i W_i and t the rounded sum_i r_i g_i / 2^19,
+// X == S - t (M mod p) (mod p).  T0 bounds t, so R = S + (T0 - t) Mp + C0
+// with C0 = -T0 Mp mod p is a non-negative representative; its bound R_max
+// follows from r_i <= m_i - 1.  The quotient estimate umulhi(R >> s2, inv2),
+// inv2 = floor(2^(s2+32) / p), undershoots R/p by less than 2^s2/p +
+// (R_max >> s2) / 2^32; when that is below 1 a single conditional subtract
+// finishes.  comb = 0 (generic two-reduction path) when a bound fails.
+// Mirrored in tests/test_rns_rules.py.
+void crt_plan_final(const RnsPlan& pl, int nmod, u64 p, rns::CrtParams& cp) {
+  cp.comb = 0;
+  if (nmod > 16) return;
+  u128 smax = 0, fmax = 0;
+  for (int i = 0; i < nmod; ++i) {
+    const u64 g = ((static_cast<u64>(pl.y[i]) << 19) + pl.mod[i] / 2) / pl.mod[i];
+    smax += static_cast<u128>(pl.mod[i] - 1) * pl.W[i];
+    fmax += static_cast<u128>(pl.mod[i] - 1) * g;
+  }
+  const u128 t0 = (fmax + (u128{1} << 18)) >> 19;
+  if (t0 >= (u128{1} << 32)) return;
+  const u64 k = static_cast<u64>((t0 * pl.Mp) % p);
+  const u64 c0 = (p - k) % p;
+  const u128 rmax = smax + t0 * pl.Mp + c0;
+  if (rmax >> 64) return;
+  int bl = 0;
+  while (bl < 128 && (rmax >> bl) != 0) ++bl;
+  const int s2 = std::max(0, bl - 31);
+  if ((u128{1} << s2) >= p) return;
+  const u128 inv2 = (u128{1} << (s2 + 32)) / p;
+  // 2^s2 / p + (R_max >> s2) / 2^32 < 1  <=>  2^(s2+32) + (R_max >> s2) p < 2^32 p
+  if ((u128{1} << (s2 + 32)) + (rmax >> s2) * p >= (static_cast<u128>(p) << 32)) return;
+  cp.comb = 1;
+  cp.T0 = static_cast<uint32_t>(t0);
+  cp.s2 = static_cast<uint32_t>(s2);
+  cp.inv2 = static_cast<uint32_t>(inv2);
+  cp.C0 = c0;
+  cp.negp = static_cast<unsigned long long>(0) - p;
+}
+
 Job make_rns_job(i64 m, i64 k, i64 n, u64 p) {
   Job j;
   j.m = m, j.k = k, j.n = n, j.p = p, j.engine = kRns;
@@ -429,6 +468,8 @@ Job make_rns_job(i64 m, i64 k, i64 n, u64 p) {
       cp.wb[i / 4][b] |= static_cast<uint32_t>(byte) << (8 * (i % 4));
     }
   }
+  crt_plan_final(pl, j.nmod, p, cp);
+  if (const char* e = std::getenv("FPMM_B200_RNS_CRT_COMB")) cp.comb = cp.comb && std::atoi(e) != 0;
   rns::PackParams& pp = j.rpp;
   pp.half_p = static_cast<double>(p / 2);
   pp.pf = static_cast<double>(p);

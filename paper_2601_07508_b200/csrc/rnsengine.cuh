@@ -104,6 +104,13 @@ struct CrtParams {
   uint32_t Mp_sh32;  // floor((M mod p) 2^32 / p)
   uint32_t mod[kMaxMod];
   uint32_t wb[kCrtGroups][kCrtPlanes];  // byte b of W_i (b < 7) / g_i (b >= 7) for the group's 4 moduli
+  // one-reduction finalisation (rns_crt_spec_kernel, host-checked bounds):
+  // R = S + (T0 - t) (M mod p) + C0 == X (mod p), R <= R_max < 2^64, and
+  // q = umulhi(R >> s2, inv2) is floor(R/p) or one less, so one conditional
+  // subtract finishes R mod p (see crt_plan_final in engine.cu)
+  int comb;
+  uint32_t T0, s2, inv2;
+  unsigned long long C0, negp;  // (p - T0 (M mod p) mod p) mod p, 2^64 - p
 };
 
 // Per-modulus constants (host: rns_plan in rules.cpp).
@@ -640,6 +647,24 @@ __device__ __forceinline__ void crt4_spec(const CrtParams& P, const uint32_t (&r
     const uint32_t g0 = a[WPL], g1 = a[WPL + 1], g2 = a[WPL + 2];
     // t = round(F / 2^19), F = g0 + 2^8 g1 + 2^16 g2 (see crt_step)
     const uint32_t tt = (g1 + (g2 << 8) + (g0 >> 8) + 1024u) >> 11;
+    if (NG <= 4 && P.comb) {
+      // R = C0 + S + (T0 - t) Mp, every term non-negative, R < 2^64
+      unsigned long long R = P.C0 + a[0];
+#pragma unroll
+      for (int b = 1; b < (WPL < 4 ? WPL : 4); ++b) R = mad_wide(a[b], 1u << (8 * b), R);
+      uint32_t hi = 0;
+#pragma unroll
+      for (int b = 4; b < WPL; ++b) hi += a[b] << (8 * (b - 4));
+      const uint32_t u = P.T0 - tt;
+      R = mad_wide(u, static_cast<uint32_t>(P.Mp), R);
+      R += static_cast<unsigned long long>(hi + u * static_cast<uint32_t>(P.Mp >> 32)) << 32;
+      const uint32_t q = __umulhi(static_cast<uint32_t>(R >> P.s2), P.inv2);
+      unsigned long long r = mad_wide(q, static_cast<uint32_t>(P.negp), R) +
+                             (static_cast<unsigned long long>(q * static_cast<uint32_t>(P.negp >> 32)) << 32);
+      r = r >= p ? r - p : r;
+      out[e] = __longlong_as_double(static_cast<long long>(r | 0x4330000000000000ull)) - 4503599627370496.0;
+      continue;
+    }
     unsigned long long sm, tmod;
     if (NG <= 4) {  // n <= 16: S = sum_i r_i W_i <= 16 * 255 * (p - 1) < 2^64
       unsigned long long S = a[0];
@@ -677,11 +702,16 @@ __device__ __forceinline__ void crt4_spec(const CrtParams& P, const uint32_t (&r
   }
 }
 
-#ifndef FPMM_B200_CRT_CW
-#define FPMM_B200_CRT_CW 8
+// columns per residue load (4, 8 or 16 bytes): the whole 16-byte chunk for up
+// to 8 moduli (more bytes in flight per thread, coalesced 512-byte warp
+// loads), 8 bytes above (register budget)
+#ifndef FPMM_B200_CRT_PREFETCH
+#define FPMM_B200_CRT_PREFETCH 1
 #endif
-constexpr int kCrtCW = FPMM_B200_CRT_CW;  // columns per residue load (4, 8 or 16 bytes)
-static_assert(kCrtCW == 4 || kCrtCW == 8 || kCrtCW == 16, "CRT load width");
+template <int NG>
+constexpr int crt_cw() {
+  return NG <= 2 ? 16 : 8;
+}
 
 template <int CW>
 struct CrtWord;
@@ -705,6 +735,7 @@ struct CrtWord<16> {
 // 128 columns of its row half in 16-column chunks ([i][half][c16][row][16 B]).
 template <int WPL, int NG>
 __global__ void __launch_bounds__(256) rns_crt_spec_kernel(const __grid_constant__ CrtParams P) {
+  constexpr int kCrtCW = crt_cw<NG>();
   using W = CrtWord<kCrtCW>;
   const int tile = blockIdx.x >> 1, rank = blockIdx.x & 1;
   const int row_in_tile = threadIdx.x % kBM, half = threadIdx.x / kBM;
@@ -717,24 +748,29 @@ __global__ void __launch_bounds__(256) rns_crt_spec_kernel(const __grid_constant
   const uint8_t* pthr = P.R + (static_cast<i64>(tile) * 2 + rank) * P.nmod * kSlotPerMod +
                         (static_cast<i64>(half) * 8 * kBM + row_in_tile) * 16;
   double* dst_row = P.C + row * P.ldc + colh;
-#pragma unroll 1
-  for (int cl = 0; cl < kNT / 2; cl += kCrtCW) {
-    if (colh + cl >= P.n) break;
+  // the residue words of chunk cl (register double buffer: the next chunk's
+  // loads are in flight while this one is reconstructed)
+  auto load = [&](int cl, uint32_t (&w)[4 * NG][kCrtCW / 4]) {
     const uint8_t* pc = pthr + (cl / 16) * (16 * kBM) + (cl % 16);
-    uint32_t w[4 * NG][kCrtCW / 4];
 #pragma unroll
     for (int i = 0; i < 4 * NG; ++i) {
       typename W::T v{};
       if (i < 4 * (NG - 1) || i < P.nmod) v = __ldg(reinterpret_cast<const typename W::T*>(pc + i * kSlotPerMod));
       W::split(v, w[i]);
     }
+  };
+  // prefetch up to 8 moduli (20-25 bits at K = 8192: 0.285 -> 0.241 ms);
+  // beyond, the second buffer costs more occupancy than it hides latency
+  // (36 bits: flat, 52 bits: 0.32 -> 0.39 ms)
+  constexpr bool kPF = FPMM_B200_CRT_PREFETCH && NG <= 2;
+  auto emit = [&](int cl, const uint32_t (&cur)[4 * NG][kCrtCW / 4]) {
 #pragma unroll
     for (int s = 0; s < kCrtCW / 4; ++s) {
       const i64 col0 = colh + cl + 4 * s;
       if (col0 >= P.n) break;
       uint32_t rw[4 * NG];
 #pragma unroll
-      for (int i = 0; i < 4 * NG; ++i) rw[i] = w[i][s];
+      for (int i = 0; i < 4 * NG; ++i) rw[i] = cur[i][s];
       double out[4];
       crt4_spec<WPL, NG>(P, rw, out);
       double* dst = dst_row + cl + 4 * s;
@@ -743,6 +779,51 @@ __global__ void __launch_bounds__(256) rns_crt_spec_kernel(const __grid_constant
         *reinterpret_cast<double2*>(dst + 2) = make_double2(out[2], out[3]);
       } else {
         for (int e = 0; e < 4 && col0 + e < P.n; ++e) dst[e] = out[e];
+      }
+    }
+  };
+  if constexpr (kPF) {
+    const int cend = static_cast<int>(min(static_cast<i64>(kNT / 2), P.n - colh));
+    uint32_t w[4 * NG][kCrtCW / 4];
+    if (cend > 0) load(0, w);
+#pragma unroll 1
+    for (int cl = 0; cl < cend; cl += kCrtCW) {
+      uint32_t cur[4 * NG][kCrtCW / 4];
+#pragma unroll
+      for (int i = 0; i < 4 * NG; ++i)
+#pragma unroll
+        for (int s = 0; s < kCrtCW / 4; ++s) cur[i][s] = w[i][s];
+      if (cl + kCrtCW < cend) load(cl + kCrtCW, w);
+      emit(cl, cur);
+    }
+  } else {
+#pragma unroll 1
+    for (int cl = 0; cl < kNT / 2; cl += kCrtCW) {
+      if (colh + cl >= P.n) break;
+      const uint8_t* pc = pthr + (cl / 16) * (16 * kBM) + (cl % 16);
+      uint32_t w[4 * NG][kCrtCW / 4];
+#pragma unroll
+      for (int i = 0; i < 4 * NG; ++i) {
+        typename W::T v{};
+        if (i < 4 * (NG - 1) || i < P.nmod) v = __ldg(reinterpret_cast<const typename W::T*>(pc + i * kSlotPerMod));
+        W::split(v, w[i]);
+      }
+#pragma unroll
+      for (int s = 0; s < kCrtCW / 4; ++s) {
+        const i64 col0 = colh + cl + 4 * s;
+        if (col0 >= P.n) break;
+        uint32_t rw[4 * NG];
+#pragma unroll
+        for (int i = 0; i < 4 * NG; ++i) rw[i] = w[i][s];
+        double out[4];
+        crt4_spec<WPL, NG>(P, rw, out);
+        double* dst = dst_row + cl + 4 * s;
+        if (col0 + 4 <= P.n && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+          *reinterpret_cast<double2*>(dst) = make_double2(out[0], out[1]);
+          *reinterpret_cast<double2*>(dst + 2) = make_double2(out[2], out[3]);
+        } else {
+          for (int e = 0; e < 4 && col0 + e < P.n; ++e) dst[e] = out[e];
+        }
       }
     }
   }

@@ -202,3 +202,77 @@ def test_crt_final_quotient_estimate_bound():
         for t in [0, 1, 4095] + [rnd.randrange(4096) for _ in range(50)]:
             qt = (t * w) >> 32
             assert 0 <= t * Mp - qt * p < 2 * p
+
+
+def crt_final_constants(p, pl):
+    """crt_plan_final() (engine.cu): T0, C0, s2, inv2 of the one-reduction
+    finalisation, or None where a bound fails (the kernel then takes the
+    two-reduction path emulated by device_crt)."""
+    if len(pl["moduli"]) > 16:
+        return None
+    gs = [((y << 19) + m // 2) // m for m, y in zip(pl["moduli"], pl["y"])]
+    smax = sum((m - 1) * W for m, W in zip(pl["moduli"], pl["W"]))
+    fmax = sum((m - 1) * g for m, g in zip(pl["moduli"], gs))
+    t0 = (fmax + (1 << 18)) >> 19
+    if t0 >= 1 << 32:
+        return None
+    c0 = (p - (t0 * pl["Mp"]) % p) % p
+    rmax = smax + t0 * pl["Mp"] + c0
+    if rmax >> 64:
+        return None
+    s2 = max(0, rmax.bit_length() - 31)
+    if (1 << s2) >= p:
+        return None
+    inv2 = (1 << (s2 + 32)) // p
+    if (1 << (s2 + 32)) + (rmax >> s2) * p >= p << 32:
+        return None
+    return {"T0": t0, "C0": c0, "s2": s2, "inv2": inv2, "rmax": rmax}
+
+
+def device_crt_comb(X, p, pl, c):
+    """rns_crt_spec_kernel's one-reduction finalisation on the residues of X,
+    in the device's u32 / u64 arithmetic."""
+    planes = [0] * 10
+    for m, y, W in zip(pl["moduli"], pl["y"], pl["W"]):
+        r = X % m
+        g = ((y << 19) + m // 2) // m
+        for b in range(10):
+            wb = (W >> (8 * b)) & 0xFF if b < 7 else (g >> (8 * (b - 7))) & 0xFF
+            planes[b] += r * wb
+    t = (planes[8] + (planes[9] << 8) + (planes[7] >> 8) + 1024) >> 11
+    assert t <= c["T0"]
+    S = sum(planes[b] << (8 * b) for b in range(7))
+    R = c["C0"] + S + (c["T0"] - t) * pl["Mp"]
+    assert R <= c["rmax"] < 1 << 64
+    q = ((R >> c["s2"]) * c["inv2"]) >> 32
+    r = (R + q * ((1 << 64) - p)) & MASK64
+    assert 0 <= r < 2 * p, (R, q)
+    return r - p if r >= p else r
+
+
+@pytest.mark.parametrize("bits", [3, 8, 20, 25, 33, 40, 48, 51, 52])
+@pytest.mark.parametrize("k", [1, 256, 8192, 32768, 66048, 262144])
+def test_one_reduction_crt_at_the_range_extremes(bits, k):
+    """The spec CRT kernel's R = S + (T0 - t) Mp + C0 path: exact X mod p at
+    the extremes of X and on random X, wherever the host enables it."""
+    p = F.prev_prime(1 << bits)
+    pl = F.rns_plan(p, k)
+    c = crt_final_constants(p, pl)
+    if c is None:
+        pytest.skip("bounds fail: two-reduction path")
+    h = p // 2
+    xmax = k * h * h
+    rng = random.Random(bits * 7 + k)
+    cases = [0, 1, -1, xmax, -xmax, xmax - 1, -xmax + 1, h * h, -h * h]
+    cases += [rng.randint(-xmax, xmax) for _ in range(300)]
+    for X in cases:
+        assert device_crt_comb(X, p, pl, c) == X % p, X
+
+
+def test_one_reduction_crt_covers_the_benchmark_configs():
+    """Every product the bench times takes the one-reduction path: the
+    8192^3 sweep (20..52 bits) and C1, C3, C4 (per K slice), C5."""
+    cfgs = [(b, 8192) for b in range(20, 53)] + [(50, 1024), (52, 32768), (48, 262144), (40, 256)]
+    for bits, k in cfgs:
+        p = F.prev_prime(1 << bits)
+        assert crt_final_constants(p, F.rns_plan(p, k)) is not None, (bits, k)
