@@ -89,7 +89,7 @@ typedef struct {
 typedef struct {
   double h2d_ms;       /* host -> device copies (host-buffer entry points)   */
   double pack_ms;      /* decomposition kernels (A and B words)              */
-  double gemm_ms;      /* product kernel(s): GEMM, epilogue and (RNS) CRT     */
+  double gemm_ms;      /* product kernel(s): GEMM and its fused epilogue      */
   double comm_ms;      /* NCCL broadcast / gather                            */
   double d2h_ms;       /* device -> host copy of C                           */
   double total_ms;     /* whole call                                         */

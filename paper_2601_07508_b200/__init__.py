@@ -369,7 +369,7 @@ RNS_MAX_MODULI = 20
 
 def rns_plan(p: int, k: int) -> dict:
     """RNS engine words for residues < p and contraction length k: the byte
-    moduli and the CRT constants of the fused epilogue (fpmm_b200_rns_plan)."""
+    moduli and the constants of the CRT reconstruction kernel (fpmm_b200_rns_plan)."""
     n = C.c_int()
     mods = (C.c_uint32 * RNS_MAX_MODULI)()
     y = (C.c_uint32 * RNS_MAX_MODULI)()

@@ -90,7 +90,10 @@ struct DevBuf {
 // and reconstruction of one run beside the tensor-core kernel of another).
 struct Workspace {
   DevBuf apack, bpack, scratch, splitws, rawb;  // rawb: the partitioner's broadcast copy of raw B
-  void release() { apack.release(), bpack.release(), scratch.release(), splitws.release(), rawb.release(); }
+  DevBuf pace;                                  // RNS pacing: k-blocks issued per CTA pair
+  void release() {
+    apack.release(), bpack.release(), scratch.release(), splitws.release(), rawb.release(), pace.release();
+  }
 };
 
 struct DeviceCtx {
@@ -758,6 +761,10 @@ int rns_splits(const Job& j, i64 rows) {
     splits = pick_splits(tiles0, 74, std::min<i64>(want, j.KB / 16), std::min<i64>(j.KB / 16, 32));
   }
   if (j.KB > j.rp.seg_kb) splits = std::max<int>(splits, (j.KB + j.rp.seg_kb - 1) / j.rp.seg_kb);
+  if (const char* e = std::getenv("FPMM_B200_RNS_SLICE_KB")) {  // experiment: K slices of at most this many k-blocks
+    const int sl = std::max(1, std::atoi(e));
+    splits = std::max<int>(splits, (j.KB + sl - 1) / sl);
+  }
   const int per = (j.KB + splits - 1) / splits;
   return (j.KB + per - 1) / per;
 }
@@ -831,6 +838,21 @@ int launch_gemm_rns_rows(const Job& j, const void* apack, const void* bpack, dou
   q.scratch = static_cast<uint8_t*>(ws.scratch.get(slots * j.nmod * rns::kSlotPerMod));
   q.group = rns::kGroup;
   if (const char* d = std::getenv("FPMM_B200_RNS_GROUP")) q.group = std::max(1, std::atoi(d));
+  // pacing (rns_kernel's producer and monitor): for passes longer than 8192 k
+  // a wave's panels (21 of 256 x k bytes) exceed L2 and the pairs drift apart
+  // unless held within 64 k-blocks of the slowest; measured: C3 32768^3 rns_kernel
+  // DRAM reads 1048 -> 328 GB and 533 -> 443 ms per product, C4 287 -> 90 GB and
+  // 57 -> 42 ms; at k = 8192 (fits L2) it only costs (sweep -3.5%):
+  // profiles/round2/ab_pace.txt.  FPMM_B200_RNS_PACE=<k-blocks> overrides (0 = off).
+  q.pace_kb = q.kb_per_split > 64 ? 64 : 0;
+  if (const char* e = std::getenv("FPMM_B200_RNS_PACE")) q.pace_kb = std::max(0, std::atoi(e));
+  q.progress = nullptr;
+  if (q.pace_kb > 0) {
+    const size_t np = grid / 2, padded = (np + 3) / 4 * 4;  // pace_min reads int4s; padding = INT_MAX-ish
+    q.progress = static_cast<int*>(ws.pace.get(sizeof(int) * padded));
+    CUDA_OK(cudaMemsetAsync(q.progress, 0x7f, sizeof(int) * padded, s));
+    CUDA_OK(cudaMemsetAsync(q.progress, 0, sizeof(int) * np, s));
+  }
   static bool configured[64] = {};
   if (!configured[dev & 63]) {
     CUDA_OK(cudaFuncSetAttribute(rns::rns_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, rns::kSmem));
@@ -893,7 +915,7 @@ int launch_gemm_rns(const Job& j, const void* apack, const void* bpack, double* 
                     cudaStream_t s, cudaEvent_t mid, Workspace& ws) {
   const i64 pair_rows = (rows + rns::kPairM - 1) / rns::kPairM;
   const size_t per_pair_row = static_cast<size_t>(j.NB) * 2 * j.nmod * rns::kSlotPerMod *
-                              std::max<i64>(1, (j.KB + j.rp.seg_kb - 1) / j.rp.seg_kb);
+                              std::max<i64>(rns_splits(j, rows), (j.KB + j.rp.seg_kb - 1) / j.rp.seg_kb);
   size_t budget = kRnsResidueBudget;
   if (const char* e = std::getenv("FPMM_B200_RNS_RESIDUE_BUDGET")) budget = std::strtoull(e, nullptr, 10);
   const i64 chunk = std::max<i64>(1, static_cast<i64>(budget / per_pair_row));

@@ -136,6 +136,12 @@ struct Params {
   int pingpong;      // 16 epilogue warps as two groups of 8 taking alternate passes (kEpiWarps == 16;
                      // one K segment per pass, not fused)
   unsigned epi_sleep_ns;  // epilogue's accumulator wait: sleep between polls (ns), 0 = suspending try_wait
+  // pacing (long K): each pair's producer publishes the k-blocks it has issued
+  // in progress[pair] and stays at most pace_kb k-blocks ahead of the slowest
+  // pair, so the pairs that share a wave's panels stream them in lockstep and
+  // the panels are read from DRAM about once (0 = off)
+  int* progress;
+  int pace_kb;
   i64 split_stride;
   unsigned long long p, mu;            // Barrett: mu = floor(2^64 / p)
   unsigned long long two32, two32_sh;  // 2^32 mod p and its Shoup quotient
@@ -919,6 +925,24 @@ __device__ __forceinline__ void commit_pair(uint64_t* bar) {
       : "memory");
 }
 
+// Pacing (long K): rank 0's producer of every pair publishes the k-blocks it
+// has issued in progress[pair] (relaxed: a hint, never a correctness
+// condition).  Warp 1 of rank 1 (idle otherwise) is the pair's monitor: it
+// keeps the minimum over all pairs in both CTAs' shared memory, and a producer
+// that is pace_kb k-blocks ahead of that minimum sleeps until the slowest pair
+// catches up (bounded: after ~2 ms of waiting it stops pacing).
+__device__ __forceinline__ void pace_publish(int* slot, int v) {
+  asm volatile("st.relaxed.gpu.global.s32 [%0], %1;\n" ::"l"(slot), "r"(v) : "memory");
+}
+__device__ __forceinline__ int pace_load(const int* slot) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(slot) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_shared_cluster(uint32_t addr, int v) {
+  asm volatile("st.shared::cluster.s32 [%0], %1;\n" ::"r"(addr), "r"(v) : "memory");
+}
+
 // The pair's work items (modulus i, item t) in order.  fused: tile-major,
 // the n moduli of tile t back to back (t = pair, pair + npairs, ...), so the
 // last pass of a tile can rebuild C from residues the pair parked itself.
@@ -961,6 +985,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
   uint64_t* tmem_full = empty + kStages;  // [2]
   uint64_t* tmem_empty = tmem_full + 2;   // [2] leader: both CTAs drained accumulator b
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  volatile int* pace_floor = reinterpret_cast<volatile int*>(tmem_slot + 1);  // monitor's min over pairs
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = cluster_rank();
@@ -968,6 +993,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
   const int total = P.MB * P.NB * P.splits;
 
   if (threadIdx.x == 0) {
+    *pace_floor = 0;
     for (int s = 0; s < kStages; ++s) {
       dev::mbar_init(&full[s], 1);
       dev::mbar_init(&empty[s], 1);
@@ -996,6 +1022,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
       // (measured and rejected: L2 evict_last/evict_first hints for A/B, -2..10%;
       // cp.async.bulk.prefetch.L2 8..64 k-blocks ahead, -9..19%)
       int g = 0;
+      bool pace = P.pace_kb > 0 && P.progress != nullptr;
       for (PassIter pi(pair); pi.valid(P, total); pi.next(P, pair, npairs, total)) {
         {
           const int i = pi.i, t = pi.t;
@@ -1007,15 +1034,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
           const int rowB = static_cast<int>(((cb * P.nmod + i) * P.KB + kb0) * (kBStage / 128));
           for (int kb = 0; kb < nkb; ++kb, ++g) {
             const int s = g % kStages;
+            if (pace && g - P.pace_kb > *pace_floor) {
+              for (int spin = 0; g - P.pace_kb > *pace_floor; ++spin) {
+                if (spin == 20000) {  // ~2 ms: a pair that never started; stop pacing
+                  pace = false;
+                  break;
+                }
+                __nanosleep(100);
+              }
+            }
             if (g >= kStages) dev::mbar_wait(&empty[s], ((g / kStages) - 1) & 1);
             if (rank == 0) dev::mbar_arrive_expect_tx(&full[s], 2 * kStageBytes);
             tma_pair_load(sA + s * kAStage, &P.tmA, rowA + kb * (kAStage / 128), &full[s]);
             tma_pair_load(sB + s * kBStage, &P.tmB, rowB + kb * (kBStage / 128), &full[s]);
+            if (pace && rank == 0 && (g & 7) == 7) pace_publish(P.progress + pair, g + 1);
           }
         }
       }
+      if (pace && rank == 0) pace_publish(P.progress + pair, 0x7fffffff);  // done: never wait for this pair
     }
   } else if (warp == 1) {
+    if (rank == 1 && P.pace_kb > 0 && P.progress != nullptr) {
+      // ---------------- pacing monitor (rank 1: warp 1 has no MMA role) ----------------
+      const uint32_t peer_floor = peer_addr(const_cast<int*>(pace_floor), 0);
+      for (int it = 0;; ++it) {
+        int v = 0x7fffffff;
+        for (int q = lane; q < npairs; q += 32) v = min(v, pace_load(P.progress + q));
+        v = __reduce_min_sync(0xffffffffu, v);
+        if (lane == 0) {
+          *pace_floor = v;
+          st_shared_cluster(peer_floor, v);
+        }
+        if (v == 0x7fffffff || it > 4000000) break;  // every pair's producer is done
+        __nanosleep(500);
+      }
+    }
     if (rank == 0 && lane == 0) {
       // ---------------- MMA issuer (leader CTA, one thread) ----------------
       constexpr uint32_t idesc = i8::instr_desc(kPairM, kNT);
