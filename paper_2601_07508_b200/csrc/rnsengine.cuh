@@ -132,7 +132,8 @@ struct Params {
   int small_t;       // seg_kb * kBK * 255^2 < 2^24: products reduce without the 16-bit split
   int flat;          // PassIter order (see there)
   int fused;         // CRT in the last modulus pass of each tile (see rns_kernel); needs splits == 1
-  int debug;         // timing experiments only (wrong C): 1 no residue stores, 2 no reduction or stores, 4 no MMAs
+  int debug;         // timing experiments only (wrong C): 1 no residue stores, 2 no reduction or stores, 4 no MMAs,
+                     // 8 MMAs do not wait for the epilogue's drain, 16 no operand loads (stage barriers only)
   int pingpong;      // 16 epilogue warps as two groups of 8 taking alternate passes (kEpiWarps == 16;
                      // one K segment per pass, not fused)
   unsigned epi_sleep_ns;  // epilogue's accumulator wait: sleep between polls (ns), 0 = suspending try_wait
@@ -956,10 +957,9 @@ struct PassIter {
   __device__ __forceinline__ void next(const Params& P, int pair, int npairs, int total) {
     if (P.fused) {  // every modulus of a tile back to back, then the pair's next tile
       if (++i == P.nmod) i = 0, t += npairs;
-    } else if (P.flat) {
-      const int g = i * total + t + npairs;
-      i = g / total;
-      t = g - i * total;
+    } else if (P.flat) {  // g = i * total + t advances by npairs
+      t += npairs;
+      while (t >= total) t -= total, ++i;
     } else {
       t += npairs;
       if (t >= total) ++i, t = pair;
@@ -1044,6 +1044,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
               }
             }
             if (g >= kStages) dev::mbar_wait(&empty[s], ((g / kStages) - 1) & 1);
+            if (P.debug & 16) {  // timing experiment: the barrier skeleton without loads
+              if (rank == 0) dev::mbar_arrive(&full[s]);
+              continue;
+            }
             if (rank == 0) dev::mbar_arrive_expect_tx(&full[s], 2 * kStageBytes);
             tma_pair_load(sA + s * kAStage, &P.tmA, rowA + kb * (kAStage / 128), &full[s]);
             tma_pair_load(sB + s * kBStage, &P.tmB, rowB + kb * (kBStage / 128), &full[s]);
@@ -1075,15 +1079,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
       int g = 0, pass = 0;
       for (PassIter pi(pair); pi.valid(P, total); pi.next(P, pair, npairs, total)) {
         {
-          const int t = pi.t;
-          const Item it = item_of(t, P);
-          const int kb0 = it.ks * P.kb_per_split;
+          // only the slice matters here (one thread on the critical path of
+          // every pass: no tile arithmetic when there is one slice)
+          const int ks = P.splits == 1 ? 0 : pi.t / (P.MB * P.NB);
+          const int kb0 = ks * P.kb_per_split;
           const int nkb = max(0, min(P.KB, kb0 + P.kb_per_split) - kb0);
-          const int nseg = max(1, (nkb + P.seg_kb - 1) / P.seg_kb);
+          const int nseg = nkb <= P.seg_kb ? 1 : (nkb + P.seg_kb - 1) / P.seg_kb;
           int kb = 0;
           for (int seg = 0; seg < nseg; ++seg, ++pass) {
             const int b = pass & 1;
-            mbar_wait_cluster(&tmem_empty[b], ((pass >> 1) & 1) ^ 1);
+            if (!(P.debug & 8)) mbar_wait_cluster(&tmem_empty[b], ((pass >> 1) & 1) ^ 1);
             i8::fence_after();
             const uint32_t tacc = tbase + b * kNT;
             const int kend = min(nkb, kb + P.seg_kb);
