@@ -18,6 +18,7 @@
 #include "i8engine.cuh"
 #include "kernels.cuh"
 #include "rnsengine.cuh"
+#include "rnstile.cuh"
 #include "verify.cuh"
 
 namespace fpmm_b200 {
@@ -726,7 +727,7 @@ int launch_gemm_i8(const Job& j, const void* apack, const void* bpack, double* C
 // 2-D uint8 tensor map over `bytes` of a packed operand viewed as 128-byte
 // rows, box 128 x (stage chunk / 128); the encoder comes from the driver
 // through the runtime (no libcuda link dependency).
-CUtensorMap chunk_map(const void* base, size_t bytes) {
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   // thread-safe one-time lookup (calls on different devices run concurrently)
   static const PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
     cudaDriverEntryPointQueryResult q{};
@@ -736,6 +737,11 @@ CUtensorMap chunk_map(const void* base, size_t bytes) {
       throw Failure(FPMM_B200_ECUDA, "cuTensorMapEncodeTiled unavailable");
     return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }();
+  return encode;
+}
+
+CUtensorMap chunk_map(const void* base, size_t bytes) {
+  const PFN_cuTensorMapEncodeTiled_v12000 encode = tensor_map_encoder();
   CUtensorMap m{};
   constexpr cuuint32_t kRows = rns::kAStage / 128;  // one stage chunk (kBStage == kAStage)
   static_assert(rns::kAStage == rns::kBStage, "A and B stage chunks share the tensor-map box");
@@ -747,6 +753,25 @@ CUtensorMap chunk_map(const void* base, size_t bytes) {
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Failure(FPMM_B200_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return m;
+}
+
+// 3-D uint8 tensor map over packed RNS B (128-column blocks, [k16][column
+// group (16)][8 columns][16 B]): 128-byte rows of one column group, 16 groups
+// per k16 slice, k16 slices; box = 8 column groups x one stage's k16 slices
+// (half of a 128-column block: rns_tile_kernel's per-CTA B).
+CUtensorMap half_block_map(const void* base, size_t bytes) {
+  const PFN_cuTensorMapEncodeTiled_v12000 encode = tensor_map_encoder();
+  CUtensorMap m{};
+  constexpr cuuint32_t kSlices = rns::kBK / 16;
+  const cuuint64_t dims[3] = {128, 16, std::max<cuuint64_t>(kSlices, bytes / 2048)};
+  const cuuint64_t strides[2] = {128, 2048};
+  const cuuint32_t box[3] = {128, 8, kSlices};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Failure(FPMM_B200_ECUDA, "cuTensorMapEncodeTiled (3-D) failed: " + std::to_string(r));
   return m;
 }
 
@@ -769,18 +794,6 @@ int rns_splits(const Job& j, i64 rows) {
   return (j.KB + per - 1) / per;
 }
 
-// The CRT in the epilogue of each tile's last modulus pass (tile-major
-// passes, no separate reconstruction kernel): opt-in with FPMM_B200_RNS_FUSED=1,
-// without split-K only.  Measured slower than rns_crt_kernel on every config
-// (8192^3 sweep -9%, C3 -32%, C5 -37%: profiles/round2/ab_fused.txt): the
-// epilogue's 8 warps per CTA run the CRT at a fraction of a full-occupancy
-// kernel's issue rate, and the per-CTA residue blocks (71 MB at n = 15) do
-// not stay in L2 next to the operand panels, so no HBM traffic is saved.
-bool rns_fused(const Job& j, i64 rows) {
-  const char* e = std::getenv("FPMM_B200_RNS_FUSED");
-  return e && std::atoi(e) != 0 && rns_splits(j, rows) == 1;
-}
-
 int launch_gemm_rns_rows(const Job& j, const void* apack, const void* bpack, double* C, i64 ldc, i64 rows,
                          cudaStream_t s, cudaEvent_t mid, Workspace& ws) {
   rns::Params q = j.rp;
@@ -795,12 +808,8 @@ int launch_gemm_rns_rows(const Job& j, const void* apack, const void* bpack, dou
   const int splits = rns_splits(j, rows);
   q.kb_per_split = (j.KB + splits - 1) / splits;
   q.splits = splits;
-  // splits == 1: the CRT runs in the epilogue of each tile's last modulus
-  // pass (tile-major passes, residues parked per CTA); otherwise the slices'
-  // residues are summed mod m_i by rns_crt_kernel after the kernel
-  q.fused = rns_fused(j, rows) ? 1 : 0;
   // two epilogue groups on alternate passes (one K segment per pass); off: FPMM_B200_RNS_PINGPONG=0
-  q.pingpong = (!q.fused && q.kb_per_split <= q.seg_kb) ? 1 : 0;
+  q.pingpong = q.kb_per_split <= q.seg_kb ? 1 : 0;
   if (const char* e = std::getenv("FPMM_B200_RNS_PINGPONG")) q.pingpong = q.pingpong && std::atoi(e) != 0;
   if (const char* e = std::getenv("FPMM_B200_RNS_DEBUG")) q.debug = std::atoi(e);
   int dev = 0;
@@ -832,9 +841,8 @@ int launch_gemm_rns_rows(const Job& j, const void* apack, const void* bpack, dou
     max_pairs[dev & 63] = std::min(clusters, sms / 2);
   }
   const unsigned grid = 2 * static_cast<unsigned>(std::max<i64>(1, std::min<i64>(items, max_pairs[dev & 63])));
-  // residue bytes: fused, one block per CTA (reused tile after tile: ~71 MB at
-  // n = 15, L2-resident); else every item's, n bytes per output element and slice
-  const size_t slots = q.fused ? static_cast<size_t>(grid) : static_cast<size_t>(items) * 2;
+  // residue bytes: every item's, n bytes per output element and slice
+  const size_t slots = static_cast<size_t>(items) * 2;
   q.scratch = static_cast<uint8_t*>(ws.scratch.get(slots * j.nmod * rns::kSlotPerMod));
   q.group = rns::kGroup;
   if (const char* d = std::getenv("FPMM_B200_RNS_GROUP")) q.group = std::max(1, std::atoi(d));
@@ -858,7 +866,7 @@ int launch_gemm_rns_rows(const Job& j, const void* apack, const void* bpack, dou
     CUDA_OK(cudaFuncSetAttribute(rns::rns_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, rns::kSmem));
     configured[dev & 63] = true;
   }
-  // the CRT constants and C: for rns_crt_kernel, or the fused epilogue
+  // the CRT constants and C
   rns::CrtParams cp = j.rcp;
   cp.R = q.scratch;
   cp.C = C;
@@ -867,12 +875,9 @@ int launch_gemm_rns_rows(const Job& j, const void* apack, const void* bpack, dou
   cp.n = j.n;
   cp.MB = q.MB, cp.NB = q.NB, cp.splits = splits, cp.group = q.group;
   const int wpl = std::max(1, (bitsize(j.p - 1) + 7) / 8);
-  q.crt = cp;
-  q.wpl = wpl;
   rns::rns_kernel<<<grid, rns::kThreads, rns::kSmem, s>>>(q);
   CUDA_OK(cudaGetLastError());
   if (mid) CUDA_OK(cudaEventRecord(mid, s));
-  if (q.fused) return 1;
   // CRT of every tile (slices summed mod m_i first) straight into C
   const i64 tiles = static_cast<i64>(q.MB) * q.NB;
   // one K slice: the kernel specialised on the plane and group counts
@@ -911,16 +916,113 @@ int launch_gemm_rns_rows(const Job& j, const void* apack, const void* bpack, dou
 // above kRnsResidueBudget the product runs in row blocks of whole pair tiles
 // that reuse one residue buffer (e.g. 65536^2 outputs at n = 11: 47 GB).
 constexpr size_t kRnsResidueBudget = size_t{8} << 30;
+
+// The on-chip CRT (rns_tile_kernel, rnstile.cuh): one exact K segment, no
+// split-K, n <= 16.  FPMM_B200_RNS_TILE=0 never uses it, =1 wherever it applies;
+// by default only where it never measured slower than parking the residues:
+// k <= 256 with n <= 8 (up to ~24 bits; 16384^2 x 256 at 20 bits: 0.89-1.00x
+// the parked time on three boxes).  At 40 bits (C5) the two are within the
+// box-to-box spread (0.91-1.11x), at 52 bits and k >= 512 the tile kernel is
+// slower (profiles/round2/tile_kernel.md).
+constexpr int kRnsTileMaxKb = 2, kRnsTileMaxMod = 8;
+bool rns_tile(const Job& j, i64 rows) {
+  if (j.nmod > rns::kTMaxMod || j.KB > j.rp.seg_kb || rns_splits(j, rows) != 1) return false;
+  const char* e = std::getenv("FPMM_B200_RNS_TILE");
+  const int mode = e ? std::atoi(e) : -1;
+  if (mode == 0) return false;
+  return mode > 0 || (j.KB <= kRnsTileMaxKb && j.nmod <= kRnsTileMaxMod);
+}
+
+template <int WPL, int NG>
+void launch_tile_kernel(const rns::Params& q, unsigned grid, size_t smem, cudaStream_t s) {
+  auto kern = rns::rns_tile_kernel<WPL, NG>;
+  static bool configured[64] = {};
+  int dev = 0;
+  CUDA_OK(cudaGetDevice(&dev));
+  if (!configured[dev & 63]) {
+    CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    configured[dev & 63] = true;
+  }
+  kern<<<grid, rns::kTThreads, smem, s>>>(q);
+}
+
+int launch_rns_tile(const Job& j, const void* apack, const void* bpack, double* C, i64 ldc, i64 rows,
+                    cudaStream_t s, cudaEvent_t mid) {
+  rns::Params q = j.rp;
+  q.apack = static_cast<const uint8_t*>(apack);
+  q.bpack = static_cast<const uint8_t*>(bpack);
+  q.tmA = chunk_map(apack, static_cast<size_t>((rows + rns::kPairM - 1) / rns::kPairM) * j.per_rb_bytes);
+  q.tmB = half_block_map(bpack, j.bpack_bytes);
+  q.C = C;
+  q.ldc = ldc;
+  q.m = rows;
+  q.MB = static_cast<int>((rows + rns::kPairM - 1) / rns::kPairM);
+  q.NB = static_cast<int>((j.n + rns::kTNT - 1) / rns::kTNT);
+  q.splits = 1;
+  q.kb_per_split = j.KB;
+  q.group = rns::kGroup;
+  if (const char* d = std::getenv("FPMM_B200_RNS_GROUP")) q.group = std::max(1, std::atoi(d));
+  // shared memory: `stages` stages of 24 KB, then as many residue planes (16 KB
+  // each) as fit, then the barriers; TMEM: as many 128-column accumulators
+  // (2..4) as the remaining planes (32 columns each) leave room for.  The most
+  // stages that keep 2 accumulators (k = 256, n = 11: 7 stages ran 3% faster than 4)
+  constexpr int kMaxSmem = 227 * 1024, kBarBytes = 256;
+  int want = rns::kTMaxStages;
+  if (const char* e = std::getenv("FPMM_B200_RNS_TILE_STAGES")) want = std::atoi(e);
+  q.naccs = 0;
+  for (q.stages = std::max(2, std::min(rns::kTMaxStages, want)); q.stages >= 2; --q.stages) {
+    q.smem_mods = std::min(j.nmod, (kMaxSmem - kBarBytes - q.stages * rns::kTStageBytes) / rns::kTResBytes);
+    q.naccs = std::min(rns::kTMaxAccs, (512 - (j.nmod - q.smem_mods) * (rns::kTNT / 4)) / rns::kTNT);
+    if (q.naccs >= 2) break;
+  }
+  if (const char* e = std::getenv("FPMM_B200_RNS_TILE_ACCS")) q.naccs = std::min(q.naccs, std::atoi(e));
+  if (q.naccs < 2) throw Failure(FPMM_B200_EERROR, "rns_tile_kernel: on-chip residues do not fit");
+  const int res_bytes = q.smem_mods * rns::kTResBytes;
+  q.res_off = q.stages * rns::kTStageBytes;
+  q.bar_off = q.res_off + res_bytes;
+  const size_t smem = static_cast<size_t>(q.bar_off) + kBarBytes;
+  rns::CrtParams cp = j.rcp;
+  cp.R = nullptr;
+  cp.C = C;
+  cp.ldc = ldc;
+  cp.m = rows;
+  cp.n = j.n;
+  cp.MB = q.MB, cp.NB = q.NB, cp.splits = 1, cp.group = q.group;
+  q.crt = cp;
+  const int wpl = std::max(1, (bitsize(j.p - 1) + 7) / 8), ng = (j.nmod + 3) / 4;
+  q.wpl = wpl;
+  int dev = 0, sms = 148;
+  CUDA_OK(cudaGetDevice(&dev));
+  CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const i64 tiles = static_cast<i64>(q.MB) * q.NB;
+  // as many pairs as rns_kernel's co-resident clusters (one CTA per SM either way)
+  const unsigned grid = 2 * static_cast<unsigned>(std::max<i64>(1, std::min<i64>(tiles, sms / 2)));
+  switch (wpl * 8 + ng) {
+#define FPMM_TILE(W, G) \
+  case W * 8 + G: launch_tile_kernel<W, G>(q, grid, smem, s); break;
+    FPMM_TILE(1, 1) FPMM_TILE(1, 2) FPMM_TILE(2, 1) FPMM_TILE(2, 2) FPMM_TILE(3, 2) FPMM_TILE(3, 3)
+    FPMM_TILE(4, 2) FPMM_TILE(4, 3) FPMM_TILE(5, 3) FPMM_TILE(5, 4) FPMM_TILE(6, 3) FPMM_TILE(6, 4)
+    FPMM_TILE(7, 4)
+#undef FPMM_TILE
+    default:
+      throw Failure(FPMM_B200_EERROR, "rns_tile_kernel: no instance for " + std::to_string(wpl) + " planes, " +
+                                          std::to_string(j.nmod) + " moduli");
+  }
+  CUDA_OK(cudaGetLastError());
+  if (mid) CUDA_OK(cudaEventRecord(mid, s));
+  return 1;
+}
+
 int launch_gemm_rns(const Job& j, const void* apack, const void* bpack, double* C, i64 ldc, i64 rows,
                     cudaStream_t s, cudaEvent_t mid, Workspace& ws) {
+  if (rns_tile(j, rows)) return launch_rns_tile(j, apack, bpack, C, ldc, rows, s, mid);
   const i64 pair_rows = (rows + rns::kPairM - 1) / rns::kPairM;
   const size_t per_pair_row = static_cast<size_t>(j.NB) * 2 * j.nmod * rns::kSlotPerMod *
                               std::max<i64>(rns_splits(j, rows), (j.KB + j.rp.seg_kb - 1) / j.rp.seg_kb);
   size_t budget = kRnsResidueBudget;
   if (const char* e = std::getenv("FPMM_B200_RNS_RESIDUE_BUDGET")) budget = std::strtoull(e, nullptr, 10);
   const i64 chunk = std::max<i64>(1, static_cast<i64>(budget / per_pair_row));
-  // (the fused CRT parks one residue block per CTA, whatever the size)
-  if (pair_rows <= chunk || rns_fused(j, rows)) return launch_gemm_rns_rows(j, apack, bpack, C, ldc, rows, s, mid, ws);
+  if (pair_rows <= chunk) return launch_gemm_rns_rows(j, apack, bpack, C, ldc, rows, s, mid, ws);
   int launches = 0;
   for (i64 pr = 0; pr < pair_rows; pr += chunk) {
     const i64 r0 = pr * rns::kPairM, rn = std::min<i64>(rows - r0, chunk * rns::kPairM);

@@ -131,11 +131,10 @@ struct Params {
   int group;         // pair-tile rows per rasterisation group
   int small_t;       // seg_kb * kBK * 255^2 < 2^24: products reduce without the 16-bit split
   int flat;          // PassIter order (see there)
-  int fused;         // CRT in the last modulus pass of each tile (see rns_kernel); needs splits == 1
   int debug;         // timing experiments only (wrong C): 1 no residue stores, 2 no reduction or stores, 4 no MMAs,
                      // 8 MMAs do not wait for the epilogue's drain, 16 no operand loads (stage barriers only)
   int pingpong;      // 16 epilogue warps as two groups of 8 taking alternate passes (kEpiWarps == 16;
-                     // one K segment per pass, not fused)
+                     // one K segment per pass)
   unsigned epi_sleep_ns;  // epilogue's accumulator wait: sleep between polls (ns), 0 = suspending try_wait
   // pacing (long K): each pair's producer publishes the k-blocks it has issued
   // in progress[pair] and stays at most pace_kb k-blocks ahead of the slowest
@@ -143,6 +142,10 @@ struct Params {
   // the panels are read from DRAM about once (0 = off)
   int* progress;
   int pace_kb;
+  // rns_tile_kernel (rnstile.cuh): pipeline stages, byte offsets of the shared
+  // residue planes and of the barriers in dynamic shared memory, residue
+  // planes held in shared memory (the rest in TMEM), TMEM accumulators
+  int stages, res_off, bar_off, smem_mods, naccs;
   i64 split_stride;
   unsigned long long p, mu;            // Barrett: mu = floor(2^64 / p)
   unsigned long long two32, two32_sh;  // 2^32 mod p and its Shoup quotient
@@ -153,8 +156,8 @@ struct Params {
   uint32_t magic[kMaxMod];  // ceil(2^32 / m): floor(s/m) = umulhi(s, magic) for s < 2^32 / m
   uint32_t g[kMaxMod];      // round(2^24 y_i / m_i)
   uint32_t w_lo[kMaxMod], w_hi[kMaxMod];  // W_i = y_i M_i mod p
-  CrtParams crt;  // fused: the reconstruction constants and C (crt.R unused)
-  int wpl;        // fused: byte planes of W_i (ceil(bits(p - 1) / 8))
+  CrtParams crt;  // rns_tile_kernel: the reconstruction constants and C (crt.R unused)
+  int wpl;        // byte planes of W_i (ceil(bits(p - 1) / 8))
 };
 
 struct PackParams {
@@ -427,9 +430,8 @@ __device__ __forceinline__ uint4* scratch_at(uint8_t* slot, int i, int half, int
 // SMALL: every product is below 2^24 (K segments of <= 258 terms, e.g. the
 // k = 256 outer-product shape), so mod_small applies to it directly.
 template <bool SMALL>
-__device__ __forceinline__ void park32(const uint32_t (&v)[32], uint32_t m, uint32_t negm, uint32_t c16, uint32_t magic,
-                                       bool acc, uint4* dst0, uint4* dst1, bool stream = true) {
-  uint32_t w[8];
+__device__ __forceinline__ void reduce32(const uint32_t (&v)[32], uint32_t negm, uint32_t c16, uint32_t magic,
+                                         uint32_t (&w)[8]) {
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     uint32_t r[4];
@@ -441,6 +443,13 @@ __device__ __forceinline__ void park32(const uint32_t (&v)[32], uint32_t m, uint
     }
     w[q] = pack4(r[0], r[1], r[2], r[3]);
   }
+}
+
+template <bool SMALL>
+__device__ __forceinline__ void park32(const uint32_t (&v)[32], uint32_t m, uint32_t negm, uint32_t c16, uint32_t magic,
+                                       bool acc, uint4* dst0, uint4* dst1) {
+  uint32_t w[8];
+  reduce32<SMALL>(v, negm, c16, magic, w);
   if (acc) {  // earlier K segments: add the parked residues mod m
     const uint4 o0 = *dst0, o1 = *dst1;
     const uint32_t o[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
@@ -456,20 +465,13 @@ __device__ __forceinline__ void park32(const uint32_t (&v)[32], uint32_t m, uint
       w[q] = word;
     }
   }
-  if (stream) {  // streaming stores: read back only by the CRT kernel
-    __stcs(dst0, make_uint4(w[0], w[1], w[2], w[3]));
-    __stcs(dst1, make_uint4(w[4], w[5], w[6], w[7]));
-  } else {  // fused: read back by this thread n - 1 passes later, kept in L2
-    *dst0 = make_uint4(w[0], w[1], w[2], w[3]);
-    *dst1 = make_uint4(w[4], w[5], w[6], w[7]);
-  }
+  // streaming stores: read back only by the CRT kernel
+  __stcs(dst0, make_uint4(w[0], w[1], w[2], w[3]));
+  __stcs(dst1, make_uint4(w[4], w[5], w[6], w[7]));
 }
 
 // The n residue words of 4-column step c (SPLIT: the slices' residues summed mod m_i).
-// NC: the read-only (non-coherent) load path, for residues parked by an
-// earlier kernel; the fused epilogue reads bytes it wrote itself in the same
-// kernel and uses plain loads.
-template <bool SPLIT, bool NC = true>
+template <bool SPLIT>
 __device__ __forceinline__ void crt_load(const CrtParams& P, const uint8_t* __restrict__ pthr, i64 slice_stride, int c,
                                          uint32_t (&rw)[kMaxMod]) {
   const uint8_t* pc = pthr + (c >> 2) * (16 * kBM) + (c & 3) * 4;
@@ -478,8 +480,7 @@ __device__ __forceinline__ void crt_load(const CrtParams& P, const uint8_t* __re
     if (i >= P.nmod) {
       rw[i] = 0;
     } else if (!SPLIT) {
-      rw[i] = NC ? __ldg(reinterpret_cast<const uint32_t*>(pc + i * kSlotPerMod))
-                 : *reinterpret_cast<const uint32_t*>(pc + i * kSlotPerMod);
+      rw[i] = __ldg(reinterpret_cast<const uint32_t*>(pc + i * kSlotPerMod));
     } else {
       uint32_t r = *reinterpret_cast<const uint32_t*>(pc + i * kSlotPerMod);
       for (int s = 1; s < P.splits; ++s) {  // add the other slices' residues mod m_i
@@ -589,31 +590,15 @@ __device__ __forceinline__ void crt_step(const CrtParams& P, int c, i64 colh, do
 // CRT of one thread's 128 columns, four per step; all n residue words of a
 // step are loaded before any is used.  (Pipelining the next step's loads
 // measured 15-20% slower: the extra registers cost a resident block per SM.)
-template <int WPL, bool SPLIT, bool NC = true>
+template <int WPL, bool SPLIT>
 __device__ __forceinline__ void crt_row(const CrtParams& P, const uint8_t* __restrict__ pthr, i64 slice_stride,
-                                        i64 colh, double* __restrict__ dst_row, int c_begin = 0,
-                                        int c_end = (kNT / 2) / 4) {
+                                        i64 colh, double* __restrict__ dst_row) {
 #pragma unroll 1
-  for (int c = c_begin; c < c_end; ++c) {
+  for (int c = 0; c < (kNT / 2) / 4; ++c) {
     if (colh + c * 4 >= P.n) break;
     uint32_t rw[kMaxMod];
-    crt_load<SPLIT, NC>(P, pthr, slice_stride, c, rw);
+    crt_load<SPLIT>(P, pthr, slice_stride, c, rw);
     crt_step<WPL>(P, c, colh, dst_row, rw);
-  }
-}
-
-// The fused epilogue's CRT: 4-column steps [c_begin, c_end) of one row half,
-// from residues this thread parked itself (runtime byte-plane count).
-__device__ __forceinline__ void crt_row_fused(const CrtParams& P, int wpl, const uint8_t* pthr, i64 colh,
-                                              double* dst_row, int c_begin, int c_end) {
-  switch (wpl) {
-    case 1: return crt_row<1, false, false>(P, pthr, 0, colh, dst_row, c_begin, c_end);
-    case 2: return crt_row<2, false, false>(P, pthr, 0, colh, dst_row, c_begin, c_end);
-    case 3: return crt_row<3, false, false>(P, pthr, 0, colh, dst_row, c_begin, c_end);
-    case 4: return crt_row<4, false, false>(P, pthr, 0, colh, dst_row, c_begin, c_end);
-    case 5: return crt_row<5, false, false>(P, pthr, 0, colh, dst_row, c_begin, c_end);
-    case 6: return crt_row<6, false, false>(P, pthr, 0, colh, dst_row, c_begin, c_end);
-    default: return crt_row<7, false, false>(P, pthr, 0, colh, dst_row, c_begin, c_end);
   }
 }
 
@@ -944,10 +929,7 @@ __device__ __forceinline__ void st_shared_cluster(uint32_t addr, int v) {
   asm volatile("st.shared::cluster.s32 [%0], %1;\n" ::"r"(addr), "r"(v) : "memory");
 }
 
-// The pair's work items (modulus i, item t) in order.  fused: tile-major,
-// the n moduli of tile t back to back (t = pair, pair + npairs, ...), so the
-// last pass of a tile can rebuild C from residues the pair parked itself.
-// flat: one sequence over i * total + t, so every pair runs the same number of items (+-1) and
+// The pair's work items (modulus i, item t) in order.  flat: one sequence over i * total + t, so every pair runs the same number of items (+-1) and
 // the pairs that share a wave's panels stay in lockstep across moduli;
 // otherwise each modulus restarts at t = pair (pairs with one item fewer per
 // modulus run ahead into the next modulus).
@@ -955,9 +937,7 @@ struct PassIter {
   int i, t;
   __device__ __forceinline__ PassIter(int pair) : i(0), t(pair) {}
   __device__ __forceinline__ void next(const Params& P, int pair, int npairs, int total) {
-    if (P.fused) {  // every modulus of a tile back to back, then the pair's next tile
-      if (++i == P.nmod) i = 0, t += npairs;
-    } else if (P.flat) {  // g = i * total + t advances by npairs
+    if (P.flat) {  // g = i * total + t advances by npairs
       t += npairs;
       while (t >= total) t -= total, ++i;
     } else {
@@ -966,8 +946,6 @@ struct PassIter {
     }
   }
   __device__ __forceinline__ bool valid(const Params& P, int total) const { return i < P.nmod && t < total; }
-  // fused order: the last modulus of the tile (its epilogue runs the CRT)
-  __device__ __forceinline__ bool last(const Params& P) const { return P.fused && i == P.nmod - 1; }
 };
 
 // The pair (cluster of 2 CTAs on neighbouring SMs) computes a 256 x 256 tile:
@@ -1113,12 +1091,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
     }
   } else {
     // ---------------- epilogue: warps 2..9 of both CTAs ----------------
-    // Pass (modulus i, tile t): T_i mod m_i is parked in a residue block.
-    // fused (opt-in, splits == 1): the block is the CTA's own, the passes of a tile
-    // run back to back, and the epilogue of its last modulus reads the n
-    // residue bytes per element back (each thread only reads bytes it wrote
-    // itself) and runs the CRT into C.  Otherwise every tile has its block in
-    // HBM and rns_crt_kernel rebuilds C after the kernel.
+    // Pass (modulus i, tile t): T_i mod m_i is parked in the tile's residue
+    // block in HBM; rns_crt_kernel rebuilds C after the kernel (the on-chip
+    // alternative is rns_tile_kernel, rnstile.cuh).
     // pingpong: warps 2..9 take the even passes (accumulator 0), 10..17 the
     // odd ones, each warp 128 columns; a group reduces and stores one pass
     // while the other drains the next, so short-K passes (k = 256: about as
@@ -1142,9 +1117,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
         const int kb0 = it.ks * P.kb_per_split;
         const int nkb = max(0, min(P.KB, kb0 + P.kb_per_split) - kb0);
         const int nseg = max(1, (nkb + P.seg_kb - 1) / P.seg_kb);
-        // fused: one residue block per CTA, reused tile after tile (L2-resident)
-        uint8_t* slot = P.scratch + ((P.fused ? static_cast<i64>(pair) : static_cast<i64>(t)) * 2 + rank) * P.nmod *
-                                        kSlotPerMod;
+        uint8_t* slot = P.scratch + (static_cast<i64>(t) * 2 + rank) * P.nmod * kSlotPerMod;
         for (int seg = 0; seg < nseg; ++seg, ++pass) {
           const int b = pass & 1;
           if (pp && b != group) continue;  // the other group's pass
@@ -1171,8 +1144,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
               const int c0 = cb + 32 * q;
               uint4* d0 = scratch_at(slot, i, half, c0 / 16, row_in_tile);
               uint4* d1 = scratch_at(slot, i, half, c0 / 16 + 1, row_in_tile);
-              if (P.small_t) park32<true>(v[q], m, nm, c16, mg, seg > 0, d0, d1, !P.fused);
-              else park32<false>(v[q], m, nm, c16, mg, seg > 0, d0, d1, !P.fused);
+              if (P.small_t) park32<true>(v[q], m, nm, c16, mg, seg > 0, d0, d1);
+              else park32<false>(v[q], m, nm, c16, mg, seg > 0, d0, d1);
             }
           } else
 #endif
@@ -1196,20 +1169,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
               if (x == 0xFFFFFFFFu) *d0 = make_uint4(x, x, x, x);
               continue;
             }
-            if (P.small_t) park32<true>(v, m, nm, c16, mg, seg > 0, d0, d1, !P.fused);
-            else park32<false>(v, m, nm, c16, mg, seg > 0, d0, d1, !P.fused);
-          }
-        }
-        if (pi.last(P)) {
-          // every modulus of this tile is parked (by this very thread, for its
-          // row and columns): rebuild C = X mod p by the CRT while the MMAs of
-          // the pair's next tile run on the other accumulator
-          const i64 row = (2 * static_cast<i64>(it.tm) + rank) * kBM + row_in_tile;
-          if (row < P.crt.m) {
-            const int cb = (col0 % (kNT / 2)) / 4;  // first 4-column step of this warp in its half
-            const i64 colh = static_cast<i64>(it.tn) * kNT + half * (kNT / 2);
-            const uint8_t* pthr = slot + (static_cast<i64>(half) * 8 * kBM + row_in_tile) * 16;
-            crt_row_fused(P.crt, P.wpl, pthr, colh, P.crt.C + row * P.crt.ldc + colh, cb, cb + wcols / 4);
+            if (P.small_t) park32<true>(v, m, nm, c16, mg, seg > 0, d0, d1);
+            else park32<false>(v, m, nm, c16, mg, seg > 0, d0, d1);
           }
         }
       }

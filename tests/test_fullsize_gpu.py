@@ -124,18 +124,15 @@ def test_c3_32768_cubed_52bit():
 
 
 def test_c3_row_blocks_forced(monkeypatch):
-    """C3's shape class through the separate-CRT path (FPMM_B200_RNS_FUSED=0)
-    with the residue budget forced small (many row blocks, ragged last block)
-    equals the fused product bitwise."""
+    """C3's shape class with the residue budget forced small (many row blocks
+    of the parked-residue path, ragged last block) equals one launch bitwise."""
     import torch
     m, k, n = 8192 + 300, 32768, 4096
     p, A, B = _inputs(m, k, n, 52)
     pl = F.plan_for_modulus(p, m, k, n)
     C1 = torch.empty((m, n), dtype=torch.float64, device="cuda")
     C2 = torch.empty((m, n), dtype=torch.float64, device="cuda")
-    monkeypatch.setenv("FPMM_B200_RNS_FUSED", "1")
     F.mw_product_device(A, B, C1, p, pl.u, pl.v, pl.lambda_, flags=F.ENGINE_RNS)
-    monkeypatch.setenv("FPMM_B200_RNS_FUSED", "0")
     monkeypatch.setenv("FPMM_B200_RNS_RESIDUE_BUDGET", str(300 << 20))
     F.mw_product_device(A, B, C2, p, pl.u, pl.v, pl.lambda_, flags=F.ENGINE_RNS)
     assert torch.equal(C1, C2)
@@ -143,20 +140,23 @@ def test_c3_row_blocks_forced(monkeypatch):
 
 
 @pytest.mark.parametrize("shape,bits", [((8192, 8192, 8192), 20), ((8192, 8192, 8192), 52), ((1000, 3000, 777), 45),
-                                        ((65536, 256, 4096), 40), ((300, 100000, 5000), 33), ((5000, 64, 300), 26)])
-def test_rns_fused_crt_equals_separate(monkeypatch, shape, bits):
-    """The CRT in the last modulus pass's epilogue (tile-major passes,
-    residues parked per CTA) gives the separate rns_crt_kernel's C bitwise,
-    on full and ragged tiles and a split-K shape (which keeps the separate CRT)."""
+                                        ((65536, 256, 4096), 40), ((300, 100000, 5000), 33), ((5000, 64, 300), 26),
+                                        ((4096, 256, 4096), 52), ((2000, 60000, 1000), 50), ((513, 129, 385), 8)])
+def test_rns_tile_crt_equals_parked(monkeypatch, shape, bits):
+    """rns_tile_kernel (residues kept on chip, CRT in the epilogue, 256 x 128
+    tiles) gives the parked-residue path's C bitwise, forced on wherever it
+    applies (FPMM_B200_RNS_TILE=1): full and ragged tiles, n = 4..16 moduli
+    (shared-memory and TMEM residue planes), k up to one exact segment, and a
+    split-K shape that keeps the parked path."""
     import torch
     m, k, n = shape
     p, A, B = _inputs(m, k, n, bits)
     pl = F.plan_for_modulus(p, m, k, n)
-    C1 = torch.empty((m, n), dtype=torch.float64, device="cuda")
-    C2 = torch.full((m, n), -1.0, dtype=torch.float64, device="cuda")
-    monkeypatch.setenv("FPMM_B200_RNS_FUSED", "1")
+    C1 = torch.full((m, n), -1.0, dtype=torch.float64, device="cuda")
+    C2 = torch.full((m, n), -2.0, dtype=torch.float64, device="cuda")
+    monkeypatch.setenv("FPMM_B200_RNS_TILE", "1")
     F.mw_product_device(A, B, C1, p, pl.u, pl.v, pl.lambda_, flags=F.ENGINE_RNS)
-    monkeypatch.setenv("FPMM_B200_RNS_FUSED", "0")
+    monkeypatch.setenv("FPMM_B200_RNS_TILE", "0")
     F.mw_product_device(A, B, C2, p, pl.u, pl.v, pl.lambda_, flags=F.ENGINE_RNS)
     assert torch.equal(C1, C2)
     assert F.verify_device(A, B, C1, p)["ok"]
