@@ -811,6 +811,11 @@ int launch_gemm_rns_rows(const Job& j, const void* apack, const void* bpack, dou
   // two epilogue groups on alternate passes (one K segment per pass); off: FPMM_B200_RNS_PINGPONG=0
   q.pingpong = q.kb_per_split <= q.seg_kb ? 1 : 0;
   if (const char* e = std::getenv("FPMM_B200_RNS_PINGPONG")) q.pingpong = q.pingpong && std::atoi(e) != 0;
+  // pingpong drain with two TMEM loads per wait: the accumulator goes back to
+  // the MMAs two load round trips earlier; short passes gain (16384^2 x 256:
+  // -6..-8% at 20/40/52 bits), k = 1024 loses 1.5% (tools/ab/ab_pp_pairs.sh)
+  q.pp_pairs = q.kb_per_split <= 4 ? 1 : 0;
+  if (const char* e = std::getenv("FPMM_B200_RNS_PP_PAIRS")) q.pp_pairs = std::atoi(e) != 0;
   if (const char* e = std::getenv("FPMM_B200_RNS_DEBUG")) q.debug = std::atoi(e);
   int dev = 0;
   CUDA_OK(cudaGetDevice(&dev));

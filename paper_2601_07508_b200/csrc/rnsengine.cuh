@@ -146,6 +146,7 @@ struct Params {
   // residue planes and of the barriers in dynamic shared memory, residue
   // planes held in shared memory (the rest in TMEM), TMEM accumulators
   int stages, res_off, bar_off, smem_mods, naccs;
+  int pp_pairs;  // pingpong drain: two 32-column TMEM loads per wait (see the epilogue)
   i64 split_stride;
   unsigned long long p, mu;            // Barrett: mu = floor(2^64 / p)
   unsigned long long two32, two32_sh;  // 2^32 mod p and its Shoup quotient
@@ -1146,6 +1147,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
               uint4* d1 = scratch_at(slot, i, half, c0 / 16 + 1, row_in_tile);
               if (P.small_t) park32<true>(v[q], m, nm, c16, mg, seg > 0, d0, d1);
               else park32<false>(v[q], m, nm, c16, mg, seg > 0, d0, d1);
+            }
+          } else if (pp && P.pp_pairs && !(P.debug & 3)) {
+            // two 32-column loads per wait: half the drain's load round trips
+            // before the release (the MMAs of pass + 2 wait for it)
+            const int cend = col0 % (kNT / 2) + wcols;
+#pragma unroll 1
+            for (int c0 = col0 % (kNT / 2); c0 < cend; c0 += 64) {
+              uint32_t v[2][32];
+              i8::tmem_ld32(tcol + c0, v[0]);
+              i8::tmem_ld32(tcol + c0 + 32, v[1]);
+              i8::tmem_wait_ld();
+              if (c0 + 64 == cend) {
+                i8::fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(leader_tmem_empty + b * 8);
+              }
+#pragma unroll
+              for (int q = 0; q < 2; ++q) {
+                uint4* d0 = scratch_at(slot, i, half, (c0 + 32 * q) / 16, row_in_tile);
+                uint4* d1 = scratch_at(slot, i, half, (c0 + 32 * q) / 16 + 1, row_in_tile);
+                if (P.small_t) park32<true>(v[q], m, nm, c16, mg, seg > 0, d0, d1);
+                else park32<false>(v[q], m, nm, c16, mg, seg > 0, d0, d1);
+              }
             }
           } else
 #endif
