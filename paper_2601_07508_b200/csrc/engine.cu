@@ -857,7 +857,8 @@ int launch_gemm_rns_rows(const Job& j, const void* apack, const void* bpack, dou
   // DRAM reads 1048 -> 328 GB and 533 -> 443 ms per product, C4 287 -> 90 GB and
   // 57 -> 42 ms; at k = 8192 (fits L2) it only costs (sweep -3.5%):
   // profiles/round2/ab_pace.txt.  FPMM_B200_RNS_PACE=<k-blocks> overrides (0 = off).
-  q.pace_kb = q.kb_per_split > 64 ? 64 : 0;
+  constexpr int kPaceKb = 8192 / rns::kBK;  // a window of 8192 k, whatever the stage depth
+  q.pace_kb = q.kb_per_split > kPaceKb ? kPaceKb : 0;
   if (const char* e = std::getenv("FPMM_B200_RNS_PACE")) q.pace_kb = std::max(0, std::atoi(e));
   q.progress = nullptr;
   if (q.pace_kb > 0) {
@@ -967,7 +968,7 @@ int launch_rns_tile(const Job& j, const void* apack, const void* bpack, double* 
   q.kb_per_split = j.KB;
   q.group = rns::kGroup;
   if (const char* d = std::getenv("FPMM_B200_RNS_GROUP")) q.group = std::max(1, std::atoi(d));
-  // shared memory: `stages` stages of 24 KB, then as many residue planes (16 KB
+  // shared memory: `stages` stages of 48 KB, then as many residue planes (16 KB
   // each) as fit, then the barriers; TMEM: as many 128-column accumulators
   // (2..4) as the remaining planes (32 columns each) leave room for.  The most
   // stages that keep 2 accumulators (k = 256, n = 11: 7 stages ran 3% faster than 4)
@@ -975,7 +976,8 @@ int launch_rns_tile(const Job& j, const void* apack, const void* bpack, double* 
   int want = rns::kTMaxStages;
   if (const char* e = std::getenv("FPMM_B200_RNS_TILE_STAGES")) want = std::atoi(e);
   q.naccs = 0;
-  for (q.stages = std::max(2, std::min(rns::kTMaxStages, want)); q.stages >= 2; --q.stages) {
+  want = std::min({want, rns::kTMaxStages, (kMaxSmem - kBarBytes) / rns::kTStageBytes});
+  for (q.stages = std::max(2, want); q.stages >= 2; --q.stages) {
     q.smem_mods = std::min(j.nmod, (kMaxSmem - kBarBytes - q.stages * rns::kTStageBytes) / rns::kTResBytes);
     q.naccs = std::min(rns::kTMaxAccs, (512 - (j.nmod - q.smem_mods) * (rns::kTNT / 4)) / rns::kTNT);
     if (q.naccs >= 2) break;

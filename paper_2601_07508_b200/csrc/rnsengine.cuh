@@ -50,15 +50,17 @@ constexpr int kNT = 256;             // columns per tile (MMA N)
 constexpr int kBH = kNT / 2;         // B columns held by each CTA of the pair
 constexpr int kPairM = 2 * kBM;      // rows per pair tile
 // k bytes per pipeline stage: 128 (four K=32 MMAs per stage barrier) ran the
-// 8192^3 residue GEMMs 9% faster than 64 (two); 256 (three 64 KB stages) was
-// ~1% faster again on the timed sweep, kept off for the deeper pipeline
+// 8192^3 residue GEMMs 9% faster than 64 (two); 256 (three 64 KB stages, eight
+// MMAs per barrier) another 2-3% at 8192^3 and 5-6% at 32768^3 / 4096 x 262144
+// x 4096, where the one thread that waits, issues and commits per stage is on
+// the critical path (profiles/round2/ab_bk256.txt)
 #ifndef FPMM_B200_RNS_BK
-#define FPMM_B200_RNS_BK 128
+#define FPMM_B200_RNS_BK 256
 #endif
 constexpr int kBK = FPMM_B200_RNS_BK;
 constexpr int kKSteps = kBK / 32;    // MMA K = 32 for kind::i8
-constexpr int kAStage = kBM * kBK;   // this CTA's 128 rows of A (16 KB)
-constexpr int kBStage = kBH * kBK;   // this CTA's 128 columns of B (16 KB)
+constexpr int kAStage = kBM * kBK;   // this CTA's 128 rows of A (32 KB)
+constexpr int kBStage = kBH * kBK;   // this CTA's 128 columns of B (32 KB)
 constexpr int kStageBytes = kAStage + kBStage;
 constexpr int kStages = 12 * 64 / kBK;  // 192 KB of stages (kBK 64, 128, 192, 256)
 #ifndef FPMM_B200_RNS_EPI_WARPS

@@ -8,8 +8,8 @@
 // (crt4_spec, the same arithmetic as the standalone kernel) writes only C.
 //
 // Per CTA (128 rows x 128 columns of the tile, TMEM lanes = rows):
-//   shared memory  `stages` pipeline stages of 24 KB (A 128 x 128 B, B 64
-//                  columns x 128 B), at most 8;
+//   shared memory  `stages` pipeline stages of 48 KB (A 128 rows x kBK bytes,
+//                  B 64 columns x kBK bytes), at most 8;
 //   shared memory  residue planes of moduli 0..smem_mods-1 (16 KB each),
 //                  [i][4-column group (32)][row (128)] words;
 //   TMEM           `naccs` (2..4) s32 accumulators of 128 columns, used in
@@ -50,7 +50,7 @@ namespace rns {
 
 constexpr int kTNT = 128;                  // pair tile columns (MMA N)
 constexpr int kTBH = kTNT / 2;             // B columns per CTA
-constexpr int kTBStage = kTBH * kBK;       // 8 KB
+constexpr int kTBStage = kTBH * kBK;       // 16 KB
 constexpr int kTStageBytes = kAStage + kTBStage;
 constexpr int kTEpiWarps = 16;             // 4 per TMEM lane quadrant, 32 columns each
 constexpr int kTThreads = 64 + 32 * kTEpiWarps;
