@@ -582,6 +582,15 @@ Job make_job(i64 m, i64 k, i64 n, u64 p, int u, int v, int engine = kDmma, bool 
   return j;
 }
 
+// RNS packers by residue form (PackParams::fp64_pairs)
+template <typename F>
+void rns_pack_mode(int mode, F&& f) {
+  switch (mode) {
+    case 0: return f.template operator()<0>();
+    default: return f.template operator()<1>();
+  }
+}
+
 void launch_pack_a(const Job& j, const double* A, i64 lda, i64 rows, void* apack, int* err,
                    cudaStream_t s) {
   if (j.engine == kRns) {
@@ -589,8 +598,10 @@ void launch_pack_a(const Job& j, const double* A, i64 lda, i64 rows, void* apack
       check_residues_kernel<<<grid_for(rows * j.k, 256), 256, 0, s>>>(A, lda, rows, j.k, j.p, err);
     const i64 mpad = ((rows + rns::kPairM - 1) / rns::kPairM) * rns::kPairM;
     const i64 items = mpad * j.KB * (rns::kBK / 16);
-    rns::pack_a_rns<<<grid_for(items, 256), 256, 0, s>>>(A, lda, rows, j.k, j.KB, mpad, j.rpp,
-                                                          static_cast<uint8_t*>(apack));
+    rns_pack_mode(j.rpp.fp64_pairs, [&]<int MODE>() {
+      rns::pack_a_rns<MODE><<<grid_for(items, 256), 256, 0, s>>>(A, lda, rows, j.k, j.KB, mpad, j.rpp,
+                                                                 static_cast<uint8_t*>(apack));
+    });
     CUDA_OK(cudaGetLastError());
     return;
   }
@@ -628,12 +639,16 @@ void launch_pack_b_rns(const Job& j, const double* B, i64 ldb, void* bpack, int*
   const bool direct = !(smem_env && std::atoi(smem_env) != 0);
   if (direct) {
     const i64 items = static_cast<i64>(nkb) * (rns::kBK / 16) * (2 * j.NB) * rns::kBH;
-    rns::pack_b_rns_direct<<<grid_for(items, 256), 256, 0, s>>>(B, ldb, j.k, j.n, j.KB, 2 * j.NB, kb0, nkb, j.rpp,
-                                                                 static_cast<uint8_t*>(bpack));
+    rns_pack_mode(j.rpp.fp64_pairs, [&]<int MODE>() {
+      rns::pack_b_rns_direct<MODE><<<grid_for(items, 256), 256, 0, s>>>(B, ldb, j.k, j.n, j.KB, 2 * j.NB, kb0, nkb,
+                                                                        j.rpp, static_cast<uint8_t*>(bpack));
+    });
   } else {
     const i64 tiles = static_cast<i64>(nkb) * (2 * j.NB) * (rns::kBH / 32);
-    rns::pack_b_rns<<<static_cast<unsigned>(std::min<i64>(std::max<i64>(tiles, 1), 148 * 32)), 128, 0, s>>>(
-        B, ldb, j.k, j.n, j.KB, 2 * j.NB, kb0, nkb, j.rpp, static_cast<uint8_t*>(bpack));
+    rns_pack_mode(j.rpp.fp64_pairs, [&]<int MODE>() {
+      rns::pack_b_rns<MODE><<<static_cast<unsigned>(std::min<i64>(std::max<i64>(tiles, 1), 148 * 32)), 128, 0, s>>>(
+          B, ldb, j.k, j.n, j.KB, 2 * j.NB, kb0, nkb, j.rpp, static_cast<uint8_t*>(bpack));
+    });
   }
   CUDA_OK(cudaGetLastError());
 }

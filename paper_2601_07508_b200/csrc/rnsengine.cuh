@@ -167,7 +167,12 @@ struct PackParams {
   double half_p;  // floor(p/2): x > half_p is centred to x - p
   double pf;      // p
   int nmod;
-  int fp64_pairs;  // residues of modulus pairs from x' mod (m_a m_b) on the FP64 pipe (residues16_pair)
+  // residues of modulus pairs from x' mod (m_a m_b) on the FP64 pipe
+  // (residues16_pair; 0 = base-256 digits and dp4a, residues16).  A form with
+  // one DFMA quotient and the rest in 32-bit integers (u = lo32(x') - q L + L)
+  // measured 0-12% slower at 8192^2 (packs are not ALU-bound there) and 3%
+  // faster at 4096 x 262144: profiles/round2/ab_packmode.txt
+  int fp64_pairs;
   double L[kMaxMod / 2], invL[kMaxMod / 2], offL[kMaxMod / 2];  // m_2j m_2j+1 (or m_2j alone), fl(1/L), 2^52 + L
   uint32_t mod[kMaxMod];
   uint32_t wlo[kMaxMod];    // bytes (256^j mod m), j = 0..3
@@ -259,9 +264,11 @@ __device__ __forceinline__ void centre16(const double (&xs)[16], const PackParam
 }
 
 // Every residue plane of one 16-element k row: out + i * plane for modulus i.
+// MODE = PackParams::fp64_pairs (compile-time: each form has its own register budget).
+template <int MODE>
 __device__ __forceinline__ void store_residue_planes(const double (&xs)[16], const PackParams& P, uint8_t* out,
                                                      i64 plane) {
-  if (P.fp64_pairs) {
+  if constexpr (MODE == 1) {
     double xc[16];
     centre16(xs, P, xc);
 #pragma unroll 1
@@ -282,6 +289,7 @@ __device__ __forceinline__ void store_residue_planes(const double (&xs)[16], con
 // A: m x k residues -> N residue planes in the canonical K-major core-matrix
 // layout.  Chunk (rb, i, kb), kAStage bytes: [k16 c (4)][row group g (16)][row (8)][16 B].
 // Thread (row, 16-element k chunk): reads 16 doubles, writes N x 16 bytes.
+template <int MODE>
 __global__ void __launch_bounds__(256) pack_a_rns(const double* __restrict__ A, i64 lda, i64 m, i64 k, int KB,
                                                   i64 mpad, const __grid_constant__ PackParams P,
                                                   uint8_t* __restrict__ out) {
@@ -318,7 +326,7 @@ __global__ void __launch_bounds__(256) pack_a_rns(const double* __restrict__ A, 
     const i64 rb = row / kBM, kb = kc / (kBK / 16);
     const int c = static_cast<int>(kc % (kBK / 16)), g = static_cast<int>((row % kBM) / 8);
     uint8_t* base = out + ((rb * P.nmod) * KB + kb) * static_cast<i64>(kAStage) + ((c * (kBM / 8) + g) * 8 + r8) * 16;
-    store_residue_planes(xs, P, base, static_cast<i64>(KB) * kAStage);
+    store_residue_planes<MODE>(xs, P, base, static_cast<i64>(KB) * kAStage);
   }
 }
 
@@ -327,6 +335,7 @@ __global__ void __launch_bounds__(256) pack_a_rns(const double* __restrict__ A, 
 // A 128-thread block transposes a 64 (k) x 32 (column) tile through shared memory.
 // k-blocks [kb_begin, kb_begin + kb_count) only (the multi-GPU path packs B's
 // k-chunks as their broadcast lands); KB is the layout's k-block count.
+template <int MODE>
 __global__ void __launch_bounds__(128) pack_b_rns(const double* __restrict__ B, i64 ldb, i64 k, i64 n, int KB,
                                                   int NB128, int kb_begin, int kb_count,
                                                   const __grid_constant__ PackParams P, uint8_t* __restrict__ out) {
@@ -355,7 +364,7 @@ __global__ void __launch_bounds__(128) pack_b_rns(const double* __restrict__ B, 
       const int nn = sb * SW + cc, g = nn / 8, r8 = nn % 8;
       uint8_t* base =
           out + ((cb * P.nmod) * KB + kb) * static_cast<i64>(kBStage) + ((q * (kBH / 8) + g) * 8 + r8) * 16;
-      store_residue_planes(xs, P, base, static_cast<i64>(KB) * kBStage);
+      store_residue_planes<MODE>(xs, P, base, static_cast<i64>(KB) * kBStage);
     }
   }
 }
@@ -364,6 +373,7 @@ __global__ void __launch_bounds__(128) pack_b_rns(const double* __restrict__ B, 
 // column) reads its 16 k values straight from B, consecutive threads walking
 // consecutive columns, so each of the 16 loads of a warp is 256 contiguous
 // bytes of one row of B; the stores are pack_a_rns's.
+template <int MODE>
 __global__ void __launch_bounds__(256) pack_b_rns_direct(const double* __restrict__ B, i64 ldb, i64 k, i64 n, int KB,
                                                          int NB128, int kb_begin, int kb_count,
                                                          const __grid_constant__ PackParams P,
@@ -388,7 +398,7 @@ __global__ void __launch_bounds__(256) pack_b_rns_direct(const double* __restric
     const i64 cb = col / kBH, kb = kc / (kBK / 16);
     const int q = static_cast<int>(kc % (kBK / 16)), nn = static_cast<int>(col % kBH), g = nn / 8, r8 = nn % 8;
     uint8_t* base = out + ((cb * P.nmod) * KB + kb) * static_cast<i64>(kBStage) + ((q * (kBH / 8) + g) * 8 + r8) * 16;
-    store_residue_planes(xs, P, base, static_cast<i64>(KB) * kBStage);
+    store_residue_planes<MODE>(xs, P, base, static_cast<i64>(KB) * kBStage);
   }
 }
 
