@@ -287,7 +287,7 @@ __device__ __forceinline__ void store_residue_planes(const double (&xs)[16], con
 }
 
 // A: m x k residues -> N residue planes in the canonical K-major core-matrix
-// layout.  Chunk (rb, i, kb), kAStage bytes: [k16 c (4)][row group g (16)][row (8)][16 B].
+// layout.  Chunk (rb, i, kb), kAStage bytes: [k16 c (kBK / 16)][row group g (16)][row (8)][16 B].
 // Thread (row, 16-element k chunk): reads 16 doubles, writes N x 16 bytes.
 template <int MODE>
 __global__ void __launch_bounds__(256) pack_a_rns(const double* __restrict__ A, i64 lda, i64 m, i64 k, int KB,
@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(256) pack_a_rns(const double* __restrict__ A, 
 }
 
 // B: k x n residues -> N residue planes of 128-column blocks, K-major.
-// Chunk (cb, i, kb), kBStage bytes: [k16 c (4)][column group (16)][column (8)][16 B].
+// Chunk (cb, i, kb), kBStage bytes: [k16 c (kBK / 16)][column group (16)][column (8)][16 B].
 // A 128-thread block transposes a 64 (k) x 32 (column) tile through shared memory.
 // k-blocks [kb_begin, kb_begin + kb_count) only (the multi-GPU path packs B's
 // k-chunks as their broadcast lands); KB is the layout's k-block count.

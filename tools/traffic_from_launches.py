@@ -57,7 +57,7 @@ def main():
     db = json.load(open(tj))
     rel = os.path.relpath(src, ROOT)
     entry = {
-        "kernel": "rns_kernel over the 8192^3 sweep (20..52 bits, 7..15 byte moduli; CTA pairs, M256 N256, 128-byte "
+        "kernel": "rns_kernel over the 8192^3 sweep (20..52 bits, 7..15 byte moduli; CTA pairs, M256 N256, 256-byte "
                   "k stages, flat pass order)",
         "dram_bytes_per_launch": round(avg),
         "algorithmic_bytes_per_launch": round(aavg),
