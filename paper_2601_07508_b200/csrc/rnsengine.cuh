@@ -72,6 +72,11 @@ constexpr int kEpiCols = 4 * kNT / kEpiWarps;        // accumulator columns per 
 static_assert(kEpiWarps == 8 || kEpiWarps == 16, "epilogue warps");
 // epilogue: drain all of a warp's accumulator columns, release, then reduce
 // (1) or release after the last 32-column load (0)
+// MMA issuer: the whole warp 1 of the leader CTA with elect.sync (1) or its
+// lane 0 alone (0)
+#ifndef FPMM_B200_RNS_MMA_WARP
+#define FPMM_B200_RNS_MMA_WARP 1
+#endif
 #ifndef FPMM_B200_RNS_DRAIN_FIRST
 #define FPMM_B200_RNS_DRAIN_FIRST 1
 #endif
@@ -916,6 +921,32 @@ __device__ __forceinline__ void tma_pair_load(void* dst, const CUtensorMap* map,
       : "memory");
 }
 // arrive on the barrier at this offset in both CTAs of the pair once the MMAs issued so far completed
+// The same from a converged warp: every lane executes the asm with identical
+// (warp-uniform) operands, so they stay in uniform registers, and the one lane
+// elect.sync picks issues the instruction (the single-thread form moved every
+// descriptor to uniform registers with R2UR inside a BRA.U.ANY loop per MMA).
+__device__ __forceinline__ void mma_i8_pair_warp(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+  const uint32_t z = 0;
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(z));
+}
+__device__ __forceinline__ void commit_pair_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
+      "}\n" ::"r"(dev::smem_u32(bar)),
+      "h"(static_cast<uint16_t>(0x3))
+      : "memory");
+}
 __device__ __forceinline__ void commit_pair(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
@@ -1064,6 +1095,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
         __nanosleep(500);
       }
     }
+#if FPMM_B200_RNS_MMA_WARP
+    if (rank == 0) {
+      // ---------------- MMA issuer (leader CTA, warp 1 converged) ----------------
+      // Every lane runs the loop, so descriptors and counters are warp-uniform
+      // and live in uniform registers; elect.sync picks the lane that issues
+      // each MMA and commit (mma_i8_pair_warp).  The descriptors are the stage
+      // bases plus byte offsets >> 4 (address field of the descriptor).
+      constexpr uint32_t idesc = i8::instr_desc(kPairM, kNT);
+      const uint64_t adesc0 = i8::smem_desc(dev::smem_u32(sA), (kBM / 8) * 128, 128);
+      const uint64_t bdesc0 = i8::smem_desc(dev::smem_u32(sB), (kBH / 8) * 128, 128);
+      const bool issue = !(P.debug & 4);
+      int g = 0, pass = 0;
+      for (PassIter pi(pair); pi.valid(P, total); pi.next(P, pair, npairs, total)) {
+        const int ks = P.splits == 1 ? 0 : pi.t / (P.MB * P.NB);
+        const int kb0 = ks * P.kb_per_split;
+        const int nkb = max(0, min(P.KB, kb0 + P.kb_per_split) - kb0);
+        const int nseg = nkb <= P.seg_kb ? 1 : (nkb + P.seg_kb - 1) / P.seg_kb;
+        int kb = 0;
+        for (int seg = 0; seg < nseg; ++seg, ++pass) {
+          const int b = pass & 1;
+          if (!(P.debug & 8)) mbar_wait_cluster(&tmem_empty[b], ((pass >> 1) & 1) ^ 1);
+          i8::fence_after();
+          const uint32_t tacc = tbase + b * kNT;
+          const int kend = min(nkb, kb + P.seg_kb);
+          const int kstart = kb;
+          for (; kb < kend; ++kb, ++g) {
+            const int s = g % kStages;
+            dev::mbar_wait(&full[s], (g / kStages) & 1);
+            i8::fence_after();
+            const uint64_t ad = adesc0 + static_cast<uint64_t>((s * kAStage) >> 4);
+            const uint64_t bd = bdesc0 + static_cast<uint64_t>((s * kBStage) >> 4);
+#pragma unroll
+            for (int tk = 0; tk < kKSteps; ++tk) {
+              if (issue)
+                mma_i8_pair_warp(tacc, ad + static_cast<uint64_t>((tk * 2 * (kBM / 8) * 128) >> 4),
+                                 bd + static_cast<uint64_t>((tk * 2 * (kBH / 8) * 128) >> 4), idesc,
+                                 (kb > kstart || tk > 0) ? 1u : 0u);
+            }
+            commit_pair_warp(&empty[s]);  // frees stage s in both CTAs
+          }
+          commit_pair_warp(&tmem_full[b]);  // accumulator b complete in both CTAs
+        }
+      }
+    }
+#else
     if (rank == 0 && lane == 0) {
       // ---------------- MMA issuer (leader CTA, one thread) ----------------
       constexpr uint32_t idesc = i8::instr_desc(kPairM, kNT);
@@ -1102,6 +1178,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
         }
       }
     }
+#endif
   } else {
     // ---------------- epilogue: warps 2..9 of both CTAs ----------------
     // Pass (modulus i, tile t): T_i mod m_i is parked in the tile's residue
