@@ -93,6 +93,30 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(z));
 }
 
+// From a converged warp: identical operands on every lane, one lane picked by
+// elect.sync issues (no per-MMA R2UR / BRA.U.ANY sequence of the one-thread form)
+__device__ __forceinline__ void mma_i8_warp(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  const uint32_t z = 0;
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %5, %5, %5}, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(z));
+}
+__device__ __forceinline__ void mma_commit_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+      "}\n" ::"r"(dev::smem_u32(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                    dev::smem_u32(bar))
@@ -427,8 +451,8 @@ __global__ void __launch_bounds__(kThreads, 1) mwi8_kernel(const __grid_constant
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer (one thread) ----------------
-    if (lane == 0) {
+    // ---------------- MMA issuer (the converged warp; elect.sync issues) ----------------
+    {
       constexpr uint32_t idesc = instr_desc(kBM, CF::kNmma);
       int g = 0, e = 0;  // stage ring position, accumulator generation
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
@@ -452,12 +476,12 @@ __global__ void __launch_bounds__(kThreads, 1) mwi8_kernel(const __grid_constant
 #pragma unroll
               for (int i = 0; i < D; ++i) {
                 const uint64_t ad = smem_desc(a0 + i * (kBM * kBK) + tk * 2 * (kBM / 8) * 128, (kBM / 8) * 128, 128);
-                mma_i8(tbase + i * NT, ad, bd, idesc, 1u);
+                mma_i8_warp(tbase + i * NT, ad, bd, idesc, 1u);
               }
             }
-            mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
+            mma_commit_warp(&empty[s]);  // frees the stage once these MMAs have read it
           }
-          mma_commit(tmem_full);    // this segment's accumulators are complete
+          mma_commit_warp(tmem_full);    // this segment's accumulators are complete
         }
       }
     }
