@@ -940,12 +940,12 @@ constexpr size_t kRnsResidueBudget = size_t{8} << 30;
 
 // The on-chip CRT (rns_tile_kernel, rnstile.cuh): one exact K segment, no
 // split-K, n <= 16.  FPMM_B200_RNS_TILE=0 never uses it, =1 wherever it applies;
-// by default only where it never measured slower than parking the residues:
-// k <= 256 with n <= 8 (up to ~24 bits; 16384^2 x 256 at 20 bits: 0.89-1.00x
-// the parked time on three boxes).  At 40 bits (C5) the two are within the
-// box-to-box spread (0.91-1.11x), at 52 bits and k >= 512 the tile kernel is
-// slower (profiles/round2/tile_kernel.md).
-constexpr int kRnsTileMaxKb = 2, kRnsTileMaxMod = 8;
+// by default at k <= 256 with n <= 12 (up to ~40 bits), where it measured
+// faster than parking the residues once both kernels issue MMAs from a
+// converged warp (C5 65536 x 256 x 65536: 30.9 against 34.4 ms, 16384^2 x 256:
+// -5% at 20 bits, -1% at 40); at 52 bits (+4%) and k = 512 (+2%) it is slower
+// (profiles/round2/tile_kernel.md).
+constexpr int kRnsTileMaxKb = 2, kRnsTileMaxMod = 12;
 bool rns_tile(const Job& j, i64 rows) {
   if (j.nmod > rns::kTMaxMod || j.KB > j.rp.seg_kb || rns_splits(j, rows) != 1) return false;
   const char* e = std::getenv("FPMM_B200_RNS_TILE");

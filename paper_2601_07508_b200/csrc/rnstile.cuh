@@ -143,9 +143,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (rank == 0 && lane == 0) {
-      // ---------------- MMA issuer (leader CTA, one thread) ----------------
+    if (rank == 0) {
+      // ---------------- MMA issuer (leader CTA, converged warp; elect.sync issues) ----------------
       constexpr uint32_t idesc = i8::instr_desc(kPairM, kTNT);
+      const uint64_t adesc0 = i8::smem_desc(dev::smem_u32(sA), (kBM / 8) * 128, 128);
+      const uint64_t bdesc0 = i8::smem_desc(dev::smem_u32(sB), (kTBH / 8) * 128, 128);
       int s = 0, round = 0, a = 0, around = 0;
       for (int t = pair; t < tiles; t += npairs) {
         for (int i = 0; i < nmod; ++i) {
@@ -155,17 +157,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads, 1)
           for (int kb = 0; kb < KB; ++kb) {
             dev::mbar_wait(&full[s], round & 1);
             i8::fence_after();
-            const uint32_t a0 = dev::smem_u32(sA + s * kAStage), b0 = dev::smem_u32(sB + s * kTBStage);
+            const uint64_t ad = adesc0 + static_cast<uint64_t>((s * kAStage) >> 4);
+            const uint64_t bd = bdesc0 + static_cast<uint64_t>((s * kTBStage) >> 4);
 #pragma unroll
-            for (int tk = 0; tk < kKSteps; ++tk) {
-              const uint64_t ad = i8::smem_desc(a0 + tk * 2 * (kBM / 8) * 128, (kBM / 8) * 128, 128);
-              const uint64_t bd = i8::smem_desc(b0 + tk * 2 * (kTBH / 8) * 128, (kTBH / 8) * 128, 128);
-              mma_i8_pair(tacc, ad, bd, idesc, (kb > 0 || tk > 0) ? 1u : 0u);
-            }
-            commit_pair(&empty[s]);  // frees stage s in both CTAs
+            for (int tk = 0; tk < kKSteps; ++tk)
+              mma_i8_pair_warp(tacc, ad + static_cast<uint64_t>((tk * 2 * (kBM / 8) * 128) >> 4),
+                               bd + static_cast<uint64_t>((tk * 2 * (kTBH / 8) * 128) >> 4), idesc,
+                               (kb > 0 || tk > 0) ? 1u : 0u);
+            commit_pair_warp(&empty[s]);  // frees stage s in both CTAs
             if (++s == S) s = 0, ++round;
           }
-          commit_pair(&tmem_full[a]);  // accumulator a complete in both CTAs
+          commit_pair_warp(&tmem_full[a]);  // accumulator a complete in both CTAs
           if (++a == NA) a = 0, ++around;
         }
       }
