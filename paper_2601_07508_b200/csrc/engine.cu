@@ -985,10 +985,12 @@ int launch_rns_tile(const Job& j, const void* apack, const void* bpack, double* 
   if (const char* d = std::getenv("FPMM_B200_RNS_GROUP")) q.group = std::max(1, std::atoi(d));
   // shared memory: `stages` stages of 48 KB, then as many residue planes (16 KB
   // each) as fit, then the barriers; TMEM: as many 128-column accumulators
-  // (2..4) as the remaining planes (32 columns each) leave room for.  The most
-  // stages that keep 2 accumulators (k = 256, n = 11: 7 stages ran 3% faster than 4)
+  // (2..4) as the remaining planes (32 columns each) leave room for.  Two
+  // stages (two k = 256 passes ahead) and the rest for residues, so more
+  // accumulators: the MMAs run further ahead while the epilogue rebuilds a
+  // tile (C5 30.5 -> 29.7 ms, 16384^2 x 256 at 20 bits -8%, tools/ab/ab_tile_stages.sh)
   constexpr int kMaxSmem = 227 * 1024, kBarBytes = 256;
-  int want = rns::kTMaxStages;
+  int want = 2;
   if (const char* e = std::getenv("FPMM_B200_RNS_TILE_STAGES")) want = std::atoi(e);
   q.naccs = 0;
   want = std::min({want, rns::kTMaxStages, (kMaxSmem - kBarBytes) / rns::kTStageBytes});
