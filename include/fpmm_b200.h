@@ -51,7 +51,8 @@ typedef enum {
  *   I8  : base-256 multiword words on tcgen05.mma.kind::i8 (int32 TMEM accumulators)
  *   RNS : byte residues modulo pairwise-coprime m_i <= 256, one kind::i8 GEMM per
  *         modulus (epilogue parks T_i mod m_i, one byte per element), then one
- *         CRT reconstruction kernel mod p
+ *         CRT reconstruction kernel mod p; for k <= 256 with <= 12 moduli the
+ *         residues stay on chip and the CRT runs in the GEMM's epilogue
  * no flag = the library default: I8 or RNS, whichever a B200 time model
  * predicts faster for (m, k, n, p) (I8 for prepared A, where n is unknown) */
 #define FPMM_B200_ENGINE_DMMA 0x10u

@@ -71,7 +71,7 @@ INPLACE_INVERSES = 0x4
 BCAST_RAW_B = 0x8
 ENGINE_DMMA = 0x10  # FP64 multiword on the FP64 tensor pipe (DMMA)
 ENGINE_I8 = 0x20    # base-256 multiword on tcgen05.mma.kind::i8 (TMEM int32 accumulators)
-ENGINE_RNS = 0x40   # byte residues mod coprime m_i <= 256, one kind::i8 GEMM per modulus, then a CRT kernel
+ENGINE_RNS = 0x40   # byte residues mod coprime m_i <= 256, one kind::i8 GEMM per modulus, then the CRT (on chip at short K)
 DMMA_EXACT_WORDS = 0x80  # FP64 engine: exactly the caller's (u,v) words (default may pick cheaper counts)
 ASYNC = 0x100
 CHECK_EXACTNESS = 0x200  # FP64 engine: verify every accumulator <= 2^53 at each reduction (shadow-replay analogue)
