@@ -139,7 +139,8 @@ struct Params {
   int small_t;       // seg_kb * kBK * 255^2 < 2^24: products reduce without the 16-bit split
   int flat;          // PassIter order (see there)
   int debug;         // timing experiments only (wrong C): 1 no residue stores, 2 no reduction or stores, 4 no MMAs,
-                     // 8 MMAs do not wait for the epilogue's drain, 16 no operand loads (stage barriers only)
+                     // 8 MMAs do not wait for the epilogue's drain, 16 no operand loads (stage barriers only);
+                     // 22 (= 16 + 4 + 2) does not complete with the converged-warp MMA issuer (not investigated)
   int pingpong;      // 16 epilogue warps as two groups of 8 taking alternate passes (kEpiWarps == 16;
                      // one K segment per pass)
   unsigned epi_sleep_ns;  // epilogue's accumulator wait: sleep between polls (ns), 0 = suspending try_wait
