@@ -26,3 +26,21 @@ def test_reference_arm_line():
     assert d["config"]["workload"] == "c1" and d["config"]["m"] == 1024
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
+
+
+@pytest.mark.gpu
+def test_b200_arm_line_c1():
+    """The GPU arm on the C1 workload (the sweep's line format at a small size): one
+    parseable <= 3 KB line, every timed product verified on the device, roofline,
+    e2e through the host API, clocks and the kernel-launch count present."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--workload", "c1", "--steps", "3",
+                          "--warmup", "3", "--no-cpu", "--no-engines"], capture_output=True, text=True, timeout=900,
+                         cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1 and len(lines[0]) <= 3072
+    d = json.loads(lines[0])
+    assert d["value"] > 0 and d["steps"] == 3 and d["warmup"] >= 3 and d["n_gpus"] == 1
+    assert d["verified"]["ok"] is True and d["verified"]["timed_products"] == d["verified"]["of"]
+    assert d["roofline"]["frac"] > 0 and d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
+    assert d["gpu_launches"] > 0 and "sm_mhz" in d["clocks"]
