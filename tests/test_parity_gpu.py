@@ -438,3 +438,4 @@ def test_cuda_graph_capture(engine):
     torch.cuda.synchronize()
     assert torch.equal(C, ref)
     assert O.freivalds(A.cpu().numpy(), B.cpu().numpy(), C.cpu().numpy(), p, trials=2) == 0
+

@@ -209,3 +209,35 @@ def test_rns_tuning_knobs_same_c(monkeypatch, knob, value):
         monkeypatch.delenv(knob)
         assert (C == ref).all(), (knob, bits)
         assert O.freivalds(A, B, C, p, trials=2) == 0
+
+
+def test_cuda_graph_capture_tile_crt():
+    """The short-K RNS path (rns_tile_kernel: residues on chip, CRT in the
+    epilogue) captured in a CUDA graph and replayed: the same C as the eager
+    call and as the u128 oracle."""
+    import torch
+    m, k, n, bits = 512, 256, 640, 40
+    p = F.prev_prime(1 << bits)
+    pl = F.plan_for_modulus(p, m, k, n)
+    A = torch.empty((m, k), dtype=torch.float64, device="cuda")
+    B = torch.empty((k, n), dtype=torch.float64, device="cuda")
+    C = torch.empty((m, n), dtype=torch.float64, device="cuda")
+    F.random_residues_device(A, p, 5)
+    F.random_residues_device(B, p, 6)
+    torch.cuda.synchronize()
+    fl = F.ASYNC | F.ENGINE_RNS
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        F.mw_product_device(A, B, C, p, pl.u, pl.v, pl.lambda_, stream=s, flags=fl)
+    torch.cuda.synchronize()
+    ref = C.clone()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        F.mw_product_device(A, B, C, p, pl.u, pl.v, pl.lambda_, stream=s, flags=fl)
+    C.zero_()
+    torch.cuda.synchronize()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(C, ref)
+    want = O.exact_mod_gemm(A.cpu().numpy(), B.cpu().numpy(), p)
+    assert (C.cpu().numpy() == want).all()
