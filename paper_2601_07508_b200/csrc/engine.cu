@@ -945,13 +945,13 @@ constexpr size_t kRnsResidueBudget = size_t{8} << 30;
 // converged warp (C5 65536 x 256 x 65536: 30.9 against 34.4 ms, 16384^2 x 256:
 // -5% at 20 bits, -1% at 40); at 52 bits (+4%) and k = 512 (+2%) it is slower
 // (profiles/round2/tile_kernel.md).
-constexpr int kRnsTileMaxKb = 2, kRnsTileMaxMod = 12;
+constexpr int kRnsTileMaxK = 256, kRnsTileMaxMod = 12;
 bool rns_tile(const Job& j, i64 rows) {
   if (j.nmod > rns::kTMaxMod || j.KB > j.rp.seg_kb || rns_splits(j, rows) != 1) return false;
   const char* e = std::getenv("FPMM_B200_RNS_TILE");
   const int mode = e ? std::atoi(e) : -1;
   if (mode == 0) return false;
-  return mode > 0 || (j.KB <= kRnsTileMaxKb && j.nmod <= kRnsTileMaxMod);
+  return mode > 0 || (j.k <= kRnsTileMaxK && j.nmod <= kRnsTileMaxMod);
 }
 
 template <int WPL, int NG>
