@@ -125,8 +125,8 @@ struct Params {
   // 2-D byte views (128-byte rows) of the packed operands for the pair TMA
   // loads; a chunk of kAStage bytes is one 128 x (kAStage / 128) box
   CUtensorMap tmA, tmB;
-  const uint8_t* apack;  // [128-row block][modulus][k-block] chunks of kAStage bytes
-  const uint8_t* bpack;  // [128-column block][modulus][k-block] chunks of kBStage bytes
+  const uint8_t* apack;  // [128-row block][k-block][modulus] chunks of kAStage bytes
+  const uint8_t* bpack;  // [128-column block][k-block][modulus] chunks of kBStage bytes
   double* C;
   uint8_t* scratch;      // residue blocks: [item][CTA rank] x nmod * kSlotPerMod bytes
   i64 ldc, m, n;
@@ -293,7 +293,10 @@ __device__ __forceinline__ void store_residue_planes(const double (&xs)[16], con
 }
 
 // A: m x k residues -> N residue planes in the canonical K-major core-matrix
-// layout.  Chunk (rb, i, kb), kAStage bytes: [k16 c (kBK / 16)][row group g (16)][row (8)][16 B].
+// layout.  Chunk (rb, kb, i), kAStage bytes: [k16 c (kBK / 16)][row group g (16)][row (8)][16 B];
+// the n moduli of a k-block are adjacent chunks, so a thread's n 16-byte stores
+// land within n * kAStage bytes (with the modulus outermost they were KB *
+// kAStage apart: 32 MB at k = 262144)
 // Thread (row, 16-element k chunk): reads 16 doubles, writes N x 16 bytes.
 template <int MODE>
 __global__ void __launch_bounds__(256) pack_a_rns(const double* __restrict__ A, i64 lda, i64 m, i64 k, int KB,
@@ -331,13 +334,13 @@ __global__ void __launch_bounds__(256) pack_a_rns(const double* __restrict__ A, 
     }
     const i64 rb = row / kBM, kb = kc / (kBK / 16);
     const int c = static_cast<int>(kc % (kBK / 16)), g = static_cast<int>((row % kBM) / 8);
-    uint8_t* base = out + ((rb * P.nmod) * KB + kb) * static_cast<i64>(kAStage) + ((c * (kBM / 8) + g) * 8 + r8) * 16;
-    store_residue_planes<MODE>(xs, P, base, static_cast<i64>(KB) * kAStage);
+    uint8_t* base = out + ((rb * KB + kb) * P.nmod) * static_cast<i64>(kAStage) + ((c * (kBM / 8) + g) * 8 + r8) * 16;
+    store_residue_planes<MODE>(xs, P, base, static_cast<i64>(kAStage));
   }
 }
 
 // B: k x n residues -> N residue planes of 128-column blocks, K-major.
-// Chunk (cb, i, kb), kBStage bytes: [k16 c (kBK / 16)][column group (16)][column (8)][16 B].
+// Chunk (cb, kb, i), kBStage bytes: [k16 c (kBK / 16)][column group (16)][column (8)][16 B].
 // A 128-thread block transposes a 64 (k) x 32 (column) tile through shared memory.
 // k-blocks [kb_begin, kb_begin + kb_count) only (the multi-GPU path packs B's
 // k-chunks as their broadcast lands); KB is the layout's k-block count.
@@ -369,8 +372,8 @@ __global__ void __launch_bounds__(128) pack_b_rns(const double* __restrict__ B, 
       for (int e = 0; e < 16; ++e) xs[e] = tile[qt * 16 + e][cc];
       const int nn = sb * SW + cc, g = nn / 8, r8 = nn % 8;
       uint8_t* base =
-          out + ((cb * P.nmod) * KB + kb) * static_cast<i64>(kBStage) + ((q * (kBH / 8) + g) * 8 + r8) * 16;
-      store_residue_planes<MODE>(xs, P, base, static_cast<i64>(KB) * kBStage);
+          out + ((cb * KB + kb) * P.nmod) * static_cast<i64>(kBStage) + ((q * (kBH / 8) + g) * 8 + r8) * 16;
+      store_residue_planes<MODE>(xs, P, base, static_cast<i64>(kBStage));
     }
   }
 }
@@ -403,8 +406,8 @@ __global__ void __launch_bounds__(256) pack_b_rns_direct(const double* __restric
     }
     const i64 cb = col / kBH, kb = kc / (kBK / 16);
     const int q = static_cast<int>(kc % (kBK / 16)), nn = static_cast<int>(col % kBH), g = nn / 8, r8 = nn % 8;
-    uint8_t* base = out + ((cb * P.nmod) * KB + kb) * static_cast<i64>(kBStage) + ((q * (kBH / 8) + g) * 8 + r8) * 16;
-    store_residue_planes<MODE>(xs, P, base, static_cast<i64>(KB) * kBStage);
+    uint8_t* base = out + ((cb * KB + kb) * P.nmod) * static_cast<i64>(kBStage) + ((q * (kBH / 8) + g) * 8 + r8) * 16;
+    store_residue_planes<MODE>(xs, P, base, static_cast<i64>(kBStage));
   }
 }
 
@@ -1053,8 +1056,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
           const int kb0 = it.ks * P.kb_per_split;
           const int nkb = max(0, min(P.KB, kb0 + P.kb_per_split) - kb0);
           const i64 rb = 2 * static_cast<i64>(it.tm) + rank, cb = 2 * static_cast<i64>(it.tn) + rank;
-          const int rowA = static_cast<int>(((rb * P.nmod + i) * P.KB + kb0) * (kAStage / 128));
-          const int rowB = static_cast<int>(((cb * P.nmod + i) * P.KB + kb0) * (kBStage / 128));
+          // chunk (block, kb, i) of the [block][k-block][modulus] layout: k-blocks nmod chunks apart
+          const int rowA = static_cast<int>(((rb * P.KB + kb0) * P.nmod + i) * (kAStage / 128));
+          const int rowB = static_cast<int>(((cb * P.KB + kb0) * P.nmod + i) * (kBStage / 128));
+          const int kstep = P.nmod * (kAStage / 128);
           for (int kb = 0; kb < nkb; ++kb, ++g) {
             const int s = g % kStages;
             if (pace && g - P.pace_kb > *pace_floor) {
@@ -1072,8 +1077,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) rns_ker
               continue;
             }
             if (rank == 0) dev::mbar_arrive_expect_tx(&full[s], 2 * kStageBytes);
-            tma_pair_load(sA + s * kAStage, &P.tmA, rowA + kb * (kAStage / 128), &full[s]);
-            tma_pair_load(sB + s * kBStage, &P.tmB, rowB + kb * (kBStage / 128), &full[s]);
+            tma_pair_load(sA + s * kAStage, &P.tmA, rowA + kb * kstep, &full[s]);
+            tma_pair_load(sB + s * kBStage, &P.tmB, rowB + kb * kstep, &full[s]);
             if (pace && rank == 0 && (g & 7) == 7) pace_publish(P.progress + pair, g + 1);
           }
         }

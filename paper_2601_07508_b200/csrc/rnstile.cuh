@@ -130,13 +130,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads, 1)
         const Item it = item_of(t, P);
         const i64 rb = 2 * static_cast<i64>(it.tm) + rank, cb = it.tn;
         for (int i = 0; i < nmod; ++i) {
-          const int rowA = static_cast<int>(((rb * nmod + i) * KB) * (kAStage / 128));
-          const int zB = static_cast<int>(((cb * nmod + i) * KB) * (kBK / 16));
+          const int rowA = static_cast<int>(((rb * KB) * nmod + i) * (kAStage / 128));
+          const int zB = static_cast<int>(((cb * KB) * nmod + i) * (kBK / 16));
           for (int kb = 0; kb < KB; ++kb) {
             if (round > 0) dev::mbar_wait(&empty[s], (round - 1) & 1);
             if (rank == 0) dev::mbar_arrive_expect_tx(&full[s], 2 * kTStageBytes);
-            tma_pair_load(sA + s * kAStage, &P.tmA, rowA + kb * (kAStage / 128), &full[s]);
-            tma_pair_load3(sB + s * kTBStage, &P.tmB, 8 * static_cast<int>(rank), zB + kb * (kBK / 16), &full[s]);
+            // [block][k-block][modulus] chunks: consecutive k-blocks are nmod chunks apart
+            tma_pair_load(sA + s * kAStage, &P.tmA, rowA + kb * nmod * (kAStage / 128), &full[s]);
+            tma_pair_load3(sB + s * kTBStage, &P.tmB, 8 * static_cast<int>(rank), zB + kb * nmod * (kBK / 16),
+                           &full[s]);
             if (++s == S) s = 0, ++round;
           }
         }
