@@ -26,10 +26,11 @@
 // No int32 product leaves the SM; the parked residues are n bytes per output
 // element.
 //
-// rns_kernel warp roles (10 warps): 0 TMA producer (2-CTA tensor-map loads
-// completing on the leader's barrier), 1 TMEM allocator + (leader only) the
-// single-thread MMA issuer, 2..9 epilogue (TMEM lane quadrant w % 4, column
-// half (w - 2) / 4).
+// rns_kernel warp roles (18 warps): 0 TMA producer (2-CTA tensor-map loads
+// completing on the leader's barrier), 1 TMEM allocator + (leader) the MMA
+// issuer, a converged warp whose elect.sync lane issues, or (rank 1) the
+// long-K pacing monitor, 2..17 epilogue (TMEM lane quadrant w % 4; two groups
+// of eight on alternate passes for one-segment passes, else 64 columns each).
 #pragma once
 
 #include <cuda.h>
