@@ -664,9 +664,11 @@ __device__ __forceinline__ void crt4_spec(const CrtParams& P, const uint32_t (&r
     const uint32_t tt = (g1 + (g2 << 8) + (g0 >> 8) + 1024u) >> 11;
     if (NG <= 4 && P.comb) {
       // R = C0 + S + (T0 - t) Mp, every term non-negative, R < 2^64
-      unsigned long long R = P.C0 + a[0];
+      // planes 0 and 1 in 32 bits (each plane < 16 255^2 < 2^20, so a0 + 2^8 a1 < 2^29):
+      // one ALU LEA instead of a 64-bit multiply-add on the FMA-heavy pipe
+      unsigned long long R = P.C0 + (WPL > 1 ? a[0] + (a[1] << 8) : a[0]);
 #pragma unroll
-      for (int b = 1; b < (WPL < 4 ? WPL : 4); ++b) R = mad_wide(a[b], 1u << (8 * b), R);
+      for (int b = 2; b < (WPL < 4 ? WPL : 4); ++b) R = mad_wide(a[b], 1u << (8 * b), R);
       uint32_t hi = 0;
 #pragma unroll
       for (int b = 4; b < WPL; ++b) hi += a[b] << (8 * (b - 4));
