@@ -409,6 +409,17 @@ void crt_plan_final(const RnsPlan& pl, int nmod, u64 p, rns::CrtParams& cp) {
   cp.inv2 = static_cast<uint32_t>(inv2);
   cp.C0 = c0;
   cp.negp = static_cast<unsigned long long>(0) - p;
+  // FP64 finalisation (crt4_spec in rns_tile_kernel, at most 5 byte planes):
+  // R_max < 2^53 keeps every partial sum exact; the byte planes are < 2^20 (n <= 16)
+  cp.fp64fin = 0;
+  if (rmax < (u128{1} << 53) && p <= (u64{1} << 40)) {
+    cp.fp64fin = 1;
+    cp.Mp_d = static_cast<double>(pl.Mp);
+    cp.C0_d = static_cast<double>(c0);
+    cp.p_d = static_cast<double>(p);
+    cp.invp_d = 1.0 / static_cast<double>(p);
+  }
+  if (const char* e = std::getenv("FPMM_B200_RNS_CRT_FP64")) cp.fp64fin = cp.fp64fin && std::atoi(e) != 0;
 }
 
 Job make_rns_job(i64 m, i64 k, i64 n, u64 p) {

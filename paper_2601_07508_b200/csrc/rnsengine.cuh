@@ -119,6 +119,10 @@ struct CrtParams {
   int comb;
   uint32_t T0, s2, inv2;
   unsigned long long C0, negp;  // (p - T0 (M mod p) mod p) mod p, 2^64 - p
+  // the same R on the FP64 pipe when R_max < 2^53 (p <= 2^40): S, (T0 - t) Mp and C0
+  // are exact doubles, R mod p = R - rint(R fl(1/p)) p (+ p when negative)
+  int fp64fin;
+  double Mp_d, C0_d, p_d, invp_d;
 };
 
 // Per-modulus constants (host: rns_plan in rules.cpp).
@@ -637,7 +641,10 @@ __device__ __forceinline__ void crt_row(const CrtParams& P, const uint8_t* __res
 
 // 4 columns -> 4 outputs mod p from the n residue words of the columns
 // (rw[i]: modulus i, bytes = columns).  Same arithmetic as crt_step.
-template <int WPL, int NG>
+// FIN64: the finalisation on the FP64 pipe where the host allows it (P.fp64fin):
+// rns_tile_kernel, whose epilogue is bound by the FMA-heavy pipe (C5 -1.2%); the
+// standalone CRT kernel is not, and ran 2-4% slower with it
+template <int WPL, int NG, bool FIN64 = false>
 __device__ __forceinline__ void crt4_spec(const CrtParams& P, const uint32_t (&rw)[4 * NG], double (&out)[4]) {
   constexpr int NP = WPL + 3;  // planes: W bytes 0..WPL-1, then g bytes 0..2
   uint32_t acc[4][NP];
@@ -662,6 +669,24 @@ __device__ __forceinline__ void crt4_spec(const CrtParams& P, const uint32_t (&r
     const uint32_t g0 = a[WPL], g1 = a[WPL + 1], g2 = a[WPL + 2];
     // t = round(F / 2^19), F = g0 + 2^8 g1 + 2^16 g2 (see crt_step)
     const uint32_t tt = (g1 + (g2 << 8) + (g0 >> 8) + 1024u) >> 11;
+    if (FIN64 && WPL <= 5 && NG <= 4 && P.fp64fin) {
+      // R = S + (T0 - t) Mp + C0 on the FP64 pipe (idle in this kernel; the
+      // integer pipes carry the dp4a planes).  Host-checked R_max < 2^53: every
+      // partial sum is a non-negative integer below R_max, so exact; q =
+      // rint(R fl(1/p)) is within 1/2 + 2^-11 of R/p, so r = R - q p (exact,
+      // |r| <= p/2 + 1) needs one conditional + p.
+      const double two52 = 4503599627370496.0, M = 6755399441055744.0;
+      double S = __hiloint2double(0x43300000, static_cast<int>(a[0])) - two52;
+#pragma unroll
+      for (int b = 1; b < WPL; ++b)
+        S = __fma_rn(__hiloint2double(0x43300000, static_cast<int>(a[b])) - two52, static_cast<double>(1ull << (8 * b)), S);
+      const double ud = __hiloint2double(0x43300000, static_cast<int>(P.T0 - tt)) - two52;
+      const double R = __fma_rn(ud, P.Mp_d, S) + P.C0_d;
+      const double q = __fma_rn(R, P.invp_d, M) - M;
+      const double r = __fma_rn(-q, P.p_d, R);
+      out[e] = r < 0.0 ? r + P.p_d : r;
+      continue;
+    }
     if (NG <= 4 && P.comb) {
       // R = C0 + S + (T0 - t) Mp, every term non-negative, R < 2^64
       // planes 0 and 1 in 32 bits (each plane < 16 255^2 < 2^20, so a0 + 2^8 a1 < 2^29):

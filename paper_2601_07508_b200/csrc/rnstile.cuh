@@ -236,7 +236,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads, 1)
 #pragma unroll
           for (int i = 0; i < 4 * NG; ++i) rw[i] = r2[i][h];
           double out[4];
-          crt4_spec<WPL, NG>(P.crt, rw, out);
+          crt4_spec<WPL, NG, true>(P.crt, rw, out);
           const i64 c = col0 + 8 * c8 + 4 * h;
           if (row < P.crt.m && c < P.crt.n) {
             double* d = dst_row + c;
