@@ -276,3 +276,64 @@ def test_one_reduction_crt_covers_the_benchmark_configs():
     for bits, k in cfgs:
         p = F.prev_prime(1 << bits)
         assert crt_final_constants(p, F.rns_plan(p, k)) is not None, (bits, k)
+
+
+def _fma(a, b, c):
+    """fma(a, b, c) in binary64: the exact a b + c rounded once to nearest even."""
+    from fractions import Fraction
+    return float(Fraction(a) * Fraction(b) + Fraction(c))
+
+
+def device_crt_fp64(X, p, pl, c):
+    """rns_tile_kernel's FP64 finalisation (crt4_spec<WPL, NG, true>, p <= 2^40,
+    R_max < 2^53) on the residues of X, with every FP64 operation rounded as on
+    the device (fma emulated exactly)."""
+    planes = [0] * 10
+    for m, y, W in zip(pl["moduli"], pl["y"], pl["W"]):
+        r = X % m
+        g = ((y << 19) + m // 2) // m
+        for b in range(10):
+            wb = (W >> (8 * b)) & 0xFF if b < 7 else (g >> (8 * (b - 7))) & 0xFF
+            planes[b] += r * wb
+    t = (planes[8] + (planes[9] << 8) + (planes[7] >> 8) + 1024) >> 11
+    wpl = max(1, ((p - 1).bit_length() + 7) // 8)
+    assert wpl <= 5 and all(planes[b] < 1 << 20 for b in range(wpl))
+    S = float(planes[0])  # 2^52 + a - 2^52: exact for a < 2^32
+    for b in range(1, wpl):
+        S = _fma(float(planes[b]), float(1 << (8 * b)), S)
+    ud = float(c["T0"] - t)
+    R = _fma(ud, float(pl["Mp"]), S) + float(c["C0"])
+    M = 6755399441055744.0
+    q = _fma(R, 1.0 / float(p), M) - M
+    r = _fma(-q, float(p), R)
+    out = r + float(p) if r < 0.0 else r
+    assert out == int(out) and 0 <= out < p
+    return int(out)
+
+
+@pytest.mark.parametrize("bits", [3, 8, 20, 25, 33, 38, 40])
+@pytest.mark.parametrize("k", [1, 64, 256, 1024, 8192])
+def test_fp64_crt_finalisation_at_the_range_extremes(bits, k):
+    """The FP64-pipe finalisation rns_tile_kernel uses for p <= 2^40: exact
+    X mod p at the extremes of X and on random X, wherever the host enables it
+    (crt_plan_final: R_max < 2^53)."""
+    p = F.prev_prime(1 << bits)
+    pl = F.rns_plan(p, k)
+    c = crt_final_constants(p, pl)
+    if c is None or c["rmax"] >= 1 << 53 or len(pl["moduli"]) > 16:
+        pytest.skip("FP64 finalisation off for this plan")
+    h = p // 2
+    xmax = k * h * h
+    rng = random.Random(bits * 11 + k)
+    cases = [0, 1, -1, xmax, -xmax, xmax - 1, -xmax + 1, h * h, -h * h]
+    cases += [rng.randint(-xmax, xmax) for _ in range(150)]
+    for X in cases:
+        assert device_crt_fp64(X, p, pl, c) == X % p, X
+
+
+def test_fp64_crt_finalisation_covers_c5():
+    """C5 (k = 256, 40 bits) and the 20..40-bit short-K shapes take the FP64 path."""
+    for bits in (20, 30, 40):
+        p = F.prev_prime(1 << bits)
+        c = crt_final_constants(p, F.rns_plan(p, 256))
+        assert c is not None and c["rmax"] < 1 << 53, bits
