@@ -193,12 +193,16 @@ def test_rns_short_k_extremes(bits, k):
 
 @pytest.mark.parametrize("knob,value", [("FPMM_B200_RNS_FLAT", "0"), ("FPMM_B200_RNS_PACK_FP64", "0"),
                                         ("FPMM_B200_RNS_PACKB_SMEM", "1"), ("FPMM_B200_RNS_EPI_SLEEP", "256"),
-                                        ("FPMM_B200_RNS_GROUP", "3")])
+                                        ("FPMM_B200_RNS_GROUP", "3"), ("FPMM_B200_RNS_TILE", "0"),
+                                        ("FPMM_B200_RNS_TILE", "1"), ("FPMM_B200_RNS_TILE_STAGES", "4"),
+                                        ("FPMM_B200_RNS_CRT_FP64", "0"), ("FPMM_B200_RNS_PP_PAIRS", "0"),
+                                        ("FPMM_B200_RNS_PINGPONG", "0"), ("FPMM_B200_RNS_PACE", "4")])
 def test_rns_tuning_knobs_same_c(monkeypatch, knob, value):
     """Every INTEGRATION.md tuning knob only changes the schedule or the
     instruction mix: C stays bit-identical to the default's (and to the oracle)."""
     rng = np.random.default_rng(11)
-    for bits, (m, k, n) in ((52, (700, 900, 600)), (21, (300, 200, 520)), (40, (256, 70, 300))):
+    for bits, (m, k, n) in ((52, (700, 900, 600)), (21, (300, 200, 520)), (40, (256, 70, 300)),
+                            (40, (600, 256, 520)), (30, (300, 3000, 260))):
         p = F.prev_prime(1 << bits)
         A = rng.integers(0, p, size=(m, k)).astype(np.float64)
         B = rng.integers(0, p, size=(k, n)).astype(np.float64)
