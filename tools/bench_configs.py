@@ -48,6 +48,12 @@ def run(name, engine, stream):
 
     once()
     torch.cuda.synchronize()
+    # let the power-capped clock recover from the previous measurement (a slow
+    # engine's long run left the next one up to 20% low)
+    import time
+    time.sleep(2.0)
+    once()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(runs):
