@@ -649,10 +649,14 @@ void launch_pack_b_rns(const Job& j, const double* B, i64 ldb, void* bpack, int*
   const char* smem_env = std::getenv("FPMM_B200_RNS_PACKB_SMEM");
   const bool direct = !(smem_env && std::atoi(smem_env) != 0);
   if (direct) {
-    const i64 items = static_cast<i64>(nkb) * (rns::kBK / 16) * (2 * j.NB) * rns::kBH;
+    // x: the padded width in blocks of 256 columns; y: k16 chunks, enough blocks for ~8 waves
+    const unsigned gx = static_cast<unsigned>((2 * j.NB * rns::kBH + 255) / 256);
+    const i64 chunks = static_cast<i64>(nkb) * (rns::kBK / 16);
+    const unsigned gy = static_cast<unsigned>(std::max<i64>(1, std::min<i64>({chunks, 65535,
+                                                                               (148 * 64 + gx - 1) / gx})));
     rns_pack_mode(j.rpp.fp64_pairs, [&]<int MODE>() {
-      rns::pack_b_rns_direct<MODE><<<grid_for(items, 256), 256, 0, s>>>(B, ldb, j.k, j.n, j.KB, 2 * j.NB, kb0, nkb,
-                                                                        j.rpp, static_cast<uint8_t*>(bpack));
+      rns::pack_b_rns_direct<MODE><<<dim3(gx, gy), 256, 0, s>>>(B, ldb, j.k, j.n, j.KB, 2 * j.NB, kb0, nkb, j.rpp,
+                                                                static_cast<uint8_t*>(bpack));
     });
   } else {
     const i64 tiles = static_cast<i64>(nkb) * (2 * j.NB) * (rns::kBH / 32);

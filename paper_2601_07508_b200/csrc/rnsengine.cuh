@@ -392,26 +392,33 @@ __global__ void __launch_bounds__(256) pack_b_rns_direct(const double* __restric
                                                          int NB128, int kb_begin, int kb_count,
                                                          const __grid_constant__ PackParams P,
                                                          uint8_t* __restrict__ out) {
-  const i64 npad = static_cast<i64>(NB128) * kBH;
+  // grid: x over 256-column groups of the padded width, y strided over k16
+  // chunks (no 64-bit division per item; a full chunk loads unconditionally)
+  const i64 col = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
   const i64 chunks = static_cast<i64>(kb_count) * (kBK / 16);
-  const i64 total = chunks * npad;
-  for (i64 idx = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
-       idx += static_cast<i64>(gridDim.x) * blockDim.x) {
-    const i64 col = idx % npad;
-    const i64 kc = static_cast<i64>(kb_begin) * (kBK / 16) + idx / npad;  // global k16 chunk
+  const i64 cb = col / kBH;
+  const int nn = static_cast<int>(col % kBH), g = nn / 8, r8 = nn % 8;
+  uint8_t* const colbase = out + (cb * KB * P.nmod) * static_cast<i64>(kBStage) + (g * 8 + r8) * 16;
+  for (i64 cq = blockIdx.y; cq < chunks; cq += gridDim.y) {
+    const i64 kc = static_cast<i64>(kb_begin) * (kBK / 16) + cq;  // global k16 chunk
     const i64 k0 = kc * 16;
     double xs[16];
     if (col < n) {
       const double* src = B + k0 * ldb + col;
+      if (k0 + 16 <= k) {
 #pragma unroll
-      for (int e = 0; e < 16; ++e) xs[e] = k0 + e < k ? __ldg(src + e * ldb) : 0.0;
+        for (int e = 0; e < 16; ++e, src += ldb) xs[e] = __ldg(src);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) xs[e] = k0 + e < k ? __ldg(src + e * ldb) : 0.0;
+      }
     } else {
 #pragma unroll
       for (int e = 0; e < 16; ++e) xs[e] = 0.0;
     }
-    const i64 cb = col / kBH, kb = kc / (kBK / 16);
-    const int q = static_cast<int>(kc % (kBK / 16)), nn = static_cast<int>(col % kBH), g = nn / 8, r8 = nn % 8;
-    uint8_t* base = out + ((cb * KB + kb) * P.nmod) * static_cast<i64>(kBStage) + ((q * (kBH / 8) + g) * 8 + r8) * 16;
+    const i64 kb = kc / (kBK / 16);
+    const int q = static_cast<int>(kc % (kBK / 16));
+    uint8_t* base = colbase + (kb * P.nmod) * static_cast<i64>(kBStage) + (q * (kBH / 8)) * 8 * 16;
     store_residue_planes<MODE>(xs, P, base, static_cast<i64>(kBStage));
   }
 }
