@@ -652,6 +652,7 @@ void launch_pack_b_rns(const Job& j, const double* B, i64 ldb, void* bpack, int*
     // x: the padded width in blocks of 256 columns; y: k16 chunks, enough blocks for ~8 waves
     const unsigned gx = static_cast<unsigned>((2 * j.NB * rns::kBH + 255) / 256);
     const i64 chunks = static_cast<i64>(nkb) * (rns::kBK / 16);
+    if (gx == 0 || chunks <= 0) return;
     const unsigned gy = static_cast<unsigned>(std::max<i64>(1, std::min<i64>({chunks, 65535,
                                                                                (148 * 64 + gx - 1) / gx})));
     rns_pack_mode(j.rpp.fp64_pairs, [&]<int MODE>() {
