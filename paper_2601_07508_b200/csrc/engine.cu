@@ -884,7 +884,7 @@ int launch_gemm_rns_rows(const Job& j, const void* apack, const void* bpack, dou
   if (const char* d = std::getenv("FPMM_B200_RNS_GROUP")) q.group = std::max(1, std::atoi(d));
   // pacing (rns_kernel's producer and monitor): for passes longer than 8192 k
   // a wave's panels (21 of 256 x k bytes) exceed L2 and the pairs drift apart
-  // unless held within 64 k-blocks of the slowest; measured: C3 32768^3 rns_kernel
+  // unless held within 8192 k of the slowest (64 k-blocks of 128 B at the time); measured: C3 32768^3 rns_kernel
   // DRAM reads 1048 -> 328 GB and 533 -> 443 ms per product, C4 287 -> 90 GB and
   // 57 -> 42 ms; at k = 8192 (fits L2) it only costs (sweep -3.5%):
   // profiles/round2/ab_pace.txt.  FPMM_B200_RNS_PACE=<k-blocks> overrides (0 = off).
