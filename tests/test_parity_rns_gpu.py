@@ -245,3 +245,26 @@ def test_cuda_graph_capture_tile_crt():
     assert torch.equal(C, ref)
     want = O.exact_mod_gemm(A.cpu().numpy(), B.cpu().numpy(), p)
     assert (C.cpu().numpy() == want).all()
+
+
+@pytest.mark.parametrize("bits", [20, 40])
+def test_tile_crt_strided_views(bits):
+    """rns_tile_kernel writes C through its leading dimension: A, B and C as
+    strided views of larger device buffers (ld > cols, odd offsets), ragged
+    m and n, against the u128 oracle; the bytes around C stay untouched."""
+    import torch
+    m, k, n = 300, 256, 200
+    p = F.prev_prime(1 << bits)
+    pl = F.plan_for_modulus(p, m, k, n)
+    Abig = torch.zeros((m, k + 40), dtype=torch.float64, device="cuda")
+    Bbig = torch.zeros((k, n + 24), dtype=torch.float64, device="cuda")
+    Cbig = torch.full((m + 3, n + 56), -7.0, dtype=torch.float64, device="cuda")
+    A, B, Cv = Abig[:, 8:8 + k], Bbig[:, 4:4 + n], Cbig[1:1 + m, 16:16 + n]
+    F.random_residues_device(Abig, p, 21)
+    F.random_residues_device(Bbig, p, 22)
+    F.mw_product_device(A, B, Cv, p, pl.u, pl.v, pl.lambda_, flags=RNS)
+    want = O.exact_mod_gemm(A.cpu().numpy(), B.cpu().numpy(), p)
+    assert (Cv.cpu().numpy() == want).all()
+    untouched = Cbig.clone()
+    untouched[1:1 + m, 16:16 + n] = -7.0
+    assert (untouched == -7.0).all()
